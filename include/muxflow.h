@@ -1,0 +1,141 @@
+/*
+ * muxflow.h -- C ABI of the B200-native MuxFlow scheduling round.
+ *
+ * The reference (/root/reference/pkg/src/muxsim) is pure Python; its hot
+ * path is `scheduler.schedule` -> `predict` for every (online, offline) pair
+ * -> `max_weight_matching` (SURVEY.md §3 stack A).  Each entry point below
+ * replaces one piece of that path; the Python host mirror in
+ * `paper_2303_13803_b200/` binds them with ctypes (see INTEGRATION.md for the
+ * binding a reference maintainer would add).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no torch types.  "_dev" pointers are CUDA
+ *     device pointers, "_host" pointers are host memory (pinned or pageable).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every function returns a status (MUX_OK = 0).  The Python layer maps
+ *     MUX_EINVAL -> ValueError/TableError and MUX_ECUDA/MUX_ENOMEM ->
+ *     SchedulingAborted, mirroring the reference's error types
+ *     (predictor.py:25-26, scheduler.py:32-33).  `mux_last_error()` returns a
+ *     thread-local message for the last failure.
+ *   - All calls are re-entrant per context; a context owns its device
+ *     workspace and must not be used from two host threads at once.
+ */
+#ifndef MUXFLOW_H
+#define MUXFLOW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MUX_OK      0
+#define MUX_EINVAL  1   /* bad argument / table / out-of-range query  */
+#define MUX_ECUDA   2   /* CUDA runtime or kernel failure             */
+#define MUX_ENOMEM  3   /* device or host allocation failure          */
+#define MUX_ELIMIT  4   /* solver iteration guard tripped (never expected) */
+
+/* Weight element types for mux_score_* outputs and mux_match inputs. */
+#define MUX_W_F64   0   /* float64 weights in [0, 1] (exact predictor values) */
+#define MUX_W_F32   1   /* float32 weights in [0, 1]                          */
+#define MUX_W_I32   2   /* int32 quantised weights rint(w * 2^qbits), qbits <= 30 */
+#define MUX_W_I64   3   /* int64 quantised weights, qbits <= 44                   */
+
+/* Scoring arithmetic. */
+#define MUX_SCORE_EXACT 0  /* float64, bit-identical to predictor.predict_point */
+#define MUX_SCORE_FAST  1  /* float32 rank-J contraction     */
+
+/* Dense prediction table: predictor.py:40-71 (PredictionTable).  values is
+ * C-order [n_online_sm][n_offline_sm][n_sm_pct], online_sm outermost.      */
+typedef struct {
+    int32_t n_online_sm;
+    int32_t n_offline_sm;
+    int32_t n_sm_pct;
+    int32_t _pad;
+    const double* online_sm;   /* host pointers */
+    const double* offline_sm;
+    const double* sm_pct;
+    const double* values;
+} mux_table_t;
+
+/* Per-solve statistics (filled by mux_match / mux_round when non-NULL). */
+typedef struct {
+    int64_t n_rows;          /* N (real online rows)                      */
+    int64_t n_cols;          /* M (real offline columns)                  */
+    int64_t n_square;        /* max(N, M): the padded square size          */
+    int64_t phases;          /* epsilon-scaling phases run                 */
+    int64_t rounds;          /* parallel bidding rounds (grid barriers)    */
+    int64_t bids;            /* accepted + rejected bids                   */
+    int64_t row_scans;       /* full weight-row reads                      */
+    int64_t tail_bids;       /* bids made in single-CTA tail mode          */
+    int64_t total_q;         /* optimal total, in quantised units          */
+    double  ms_score;        /* device time of the scoring kernel(s)       */
+    double  ms_match;        /* device time of the auction                 */
+    int64_t launches;        /* kernel launches issued by the call         */
+} mux_stats_t;
+
+typedef struct mux_ctx mux_ctx_t;
+
+/* Library identity / version. */
+const char* mux_version(void);
+/* Thread-local message describing the last non-OK status. */
+const char* mux_last_error(void);
+
+/* Create a context bound to CUDA device `device` (workspace grows on demand). */
+int mux_ctx_create(int device, mux_ctx_t** out);
+int mux_ctx_destroy(mux_ctx_t* ctx);
+
+/* Validate a table exactly like PredictionTable.__post_init__
+ * (predictor.py:29-71): axes non-empty, in [0,1], strictly increasing;
+ * values finite, in [0,1], non-decreasing along sm_pct within 1e-12. */
+int mux_table_validate(const mux_table_t* table);
+
+/*
+ * Pair scoring (replaces the N x M predict() loop, scheduler.py:172-180, and
+ * predictor.py:85-118).  x_dev / share_dev: float64 [n] (online peak SM
+ * activity, granted share), y_dev: float64 [m] (offline SM demand) -- DEVICE
+ * pointers.  Output out_dev is row-major [n][ldo] of type wtype; quantised
+ * outputs apply the reference edge rule first (w < 1e-6 -> 0,
+ * matching.py:19, 159-162).  Coordinates outside [0,1] -> MUX_EINVAL
+ * (predictor.py:93-96), checked on the device.
+ */
+int mux_score_table(mux_ctx_t* ctx, const mux_table_t* table,
+                    const double* x_dev, const double* share_dev, int64_t n,
+                    const double* y_dev, int64_t m,
+                    int mode, int wtype, int qbits,
+                    void* out_dev, int64_t ldo, void* stream);
+
+/*
+ * Maximum-weight bipartite matching on non-negative integer weights
+ * (replaces max_weight_matching, matching.py:148-208, minus the tie
+ * canonicalisation).  Wq_dev: row-major [n][ldw] of wtype MUX_W_I32 or
+ * MUX_W_I64 (0 = missing edge).  Solves the reference's zero-padded square
+ * problem exactly (epsilon-scaling auction to epsilon = 1 on weights scaled by
+ * max(n, m) + 1).  col_of_row_out: int32 [n], -1 when the row is unmatched or
+ * matched through a zero-weight / padding edge (the reference never emits
+ * those, matching.py:201-208); may be a host or device pointer
+ * (`out_on_host`).  *total_q receives the optimal total in quantised units.
+ */
+int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype,
+              int64_t n, int64_t m, int64_t ldw,
+              int32_t* col_of_row_out, int out_on_host,
+              int64_t* total_q, mux_stats_t* stats, void* stream);
+
+/*
+ * One fused scheduling round from HOST feature arrays (the call the
+ * reference's `_matching_policy_schedule` makes per round, scheduler.py:143-194):
+ * H2D copy of (x, share, y), exact scoring into quantised weights, auction,
+ * D2H copy of col_of_row.  Rows with share <= 0 must already be filtered by
+ * the caller (scheduler.py:164-165), as must inadmissible columns
+ * (scheduler.py:138-140).
+ */
+int mux_round(mux_ctx_t* ctx, const mux_table_t* table,
+              const double* x_host, const double* share_host, int64_t n,
+              const double* y_host, int64_t m, int qbits,
+              int32_t* col_of_row_host, int64_t* total_q,
+              mux_stats_t* stats, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MUXFLOW_H */

@@ -1,0 +1,220 @@
+// C ABI entry points (include/muxflow.h).  Host-side argument checking,
+// context / workspace management, and the fused per-round path.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+int mux_score_table_impl(mux_ctx_t* ctx, const mux_table_t* tb, const double* x, const double* s,
+                         int64_t n, const double* y, int64_t m, int mode, int wtype, int qbits,
+                         void* out, int64_t ldo, cudaStream_t st, int64_t* launches);
+int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
+                   int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
+                   int theta, int tail_max);
+
+namespace mux {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+// Read back and clear the device error flags; maps a range error to EINVAL.
+static int check_flags(mux_ctx_t* ctx, cudaStream_t st) {
+    uint32_t f = 0;
+    MUX_CUDA_TRY(cudaMemcpyAsync(&f, ctx->flags.ptr, sizeof(f), cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    if (f) MUX_CUDA_TRY(cudaMemsetAsync(ctx->flags.ptr, 0, sizeof(uint32_t), st));
+    if (f & kErrQueryRange) { set_error("query coordinate outside [0, 1]"); return MUX_EINVAL; }
+    return MUX_OK;
+}
+
+static int pinned_ensure(mux_ctx_t* ctx, size_t bytes) {
+    if (bytes <= ctx->pinned_bytes) return MUX_OK;
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    size_t cap = bytes + bytes / 4 + 4096;
+    MUX_CUDA_TRY(cudaMallocHost(&ctx->pinned, cap));
+    ctx->pinned_bytes = cap;
+    return MUX_OK;
+}
+}  // namespace mux
+
+using namespace mux;
+
+extern "C" {
+
+const char* mux_version(void) { return "muxflow-b200 0.1 (sm_100a)"; }
+const char* mux_last_error(void) { return g_last_error.c_str(); }
+
+int mux_ctx_create(int device, mux_ctx_t** out) {
+    if (!out) { set_error("mux_ctx_create: null out"); return MUX_EINVAL; }
+    *out = nullptr;
+    int ndev = 0;
+    MUX_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) { set_error("mux_ctx_create: bad device"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    MUX_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        set_error("muxflow is built for sm_100a (B200); device is sm_" + std::to_string(prop.major * 10 + prop.minor));
+        return MUX_ECUDA;
+    }
+    mux_ctx_t* c = new mux_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    int rc = c->flags.ensure(256);
+    if (rc != MUX_OK) { delete c; return rc; }
+    if (cudaMemset(c->flags.ptr, 0, 256) != cudaSuccess) { delete c; set_error("memset"); return MUX_ECUDA; }
+    *out = c;
+    return MUX_OK;
+}
+
+int mux_ctx_destroy(mux_ctx_t* ctx) {
+    if (!ctx) return MUX_OK;
+    cudaSetDevice(ctx->device);
+    for (DevBuf* b : {&ctx->table, &ctx->rowfeat, &ctx->colfeat, &ctx->flags, &ctx->feat_in, &ctx->wq,
+                      &ctx->colout, &ctx->auc})
+        b->release();
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    delete ctx;
+    return MUX_OK;
+}
+
+// predictor.py:29-37 (_check_axis) and 56-71 (PredictionTable.__post_init__).
+int mux_table_validate(const mux_table_t* t) {
+    if (!t) { set_error("null table"); return MUX_EINVAL; }
+    const int32_t dims[3] = {t->n_online_sm, t->n_offline_sm, t->n_sm_pct};
+    const double* axes[3] = {t->online_sm, t->offline_sm, t->sm_pct};
+    const char* names[3] = {"online_sm", "offline_sm", "sm_pct"};
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] <= 0 || !axes[a]) { set_error(std::string("axis ") + names[a] + " is empty"); return MUX_EINVAL; }
+        for (int k = 0; k < dims[a]; ++k) {
+            const double v = axes[a][k];
+            if (!(v >= 0.0 && v <= 1.0)) { set_error(std::string("axis ") + names[a] + " knot outside [0, 1]"); return MUX_EINVAL; }
+            if (k > 0 && !(axes[a][k - 1] < v)) { set_error(std::string("axis ") + names[a] + " knots not strictly increasing"); return MUX_EINVAL; }
+        }
+    }
+    if (!t->values) { set_error("table values missing"); return MUX_EINVAL; }
+    const int64_t nv = (int64_t)dims[0] * dims[1] * dims[2];
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t e = 0; e < nv; ++e) {
+        const double v = t->values[e];
+        if (!std::isfinite(v)) { set_error("table contains non-finite values"); return MUX_EINVAL; }
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+    if (lo < 0.0 || hi > 1.0) { set_error("table values outside [0, 1]"); return MUX_EINVAL; }
+    if (dims[2] > 1) {
+        double dmin = INFINITY;
+        for (int64_t e = 0; e < nv; e += dims[2])
+            for (int k = 1; k < dims[2]; ++k) {
+                const double d = t->values[e + k] - t->values[e + k - 1];
+                dmin = d < dmin ? d : dmin;
+            }
+        if (dmin < -1e-12) { set_error("values decrease along the sm_pct axis"); return MUX_EINVAL; }
+    }
+    return MUX_OK;
+}
+
+int mux_score_table(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev, const double* share_dev,
+                    int64_t n, const double* y_dev, int64_t m, int mode, int wtype, int qbits, void* out_dev,
+                    int64_t ldo, void* stream) {
+    if (!ctx) { set_error("null context"); return MUX_EINVAL; }
+    MUX_TRY(mux_table_validate(table));
+    if (n < 0 || m < 0 || ldo < m) { set_error("mux_score_table: bad shape"); return MUX_EINVAL; }
+    if (mode != MUX_SCORE_EXACT && mode != MUX_SCORE_FAST) { set_error("bad mode"); return MUX_EINVAL; }
+    if (wtype < MUX_W_F64 || wtype > MUX_W_I64) { set_error("bad wtype"); return MUX_EINVAL; }
+    const int maxbits = wtype == MUX_W_I32 ? 30 : 52;
+    if ((wtype == MUX_W_I32 || wtype == MUX_W_I64) && (qbits < 0 || qbits > maxbits)) {
+        set_error("qbits out of range for the output type");
+        return MUX_EINVAL;
+    }
+    const int vec = (wtype == MUX_W_I32 || wtype == MUX_W_F32) ? 4 : 2;
+    if (n > 0 && ((ldo % vec) != 0 || (reinterpret_cast<uintptr_t>(out_dev) & 15))) {
+        set_error("mux_score_table: output rows must be 16-byte aligned");
+        return MUX_EINVAL;
+    }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int64_t launches = 0;
+    MUX_TRY(mux_score_table_impl(ctx, table, x_dev, share_dev, n, y_dev, m, mode, wtype, qbits, out_dev, ldo, st, &launches));
+    return check_flags(ctx, st);
+}
+
+int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t m, int64_t ldw,
+              int32_t* col_of_row_out, int out_on_host, int64_t* total_q, mux_stats_t* stats, void* stream) {
+    if (!ctx) { set_error("null context"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t* col_dev = col_of_row_out;
+    if (out_on_host) {
+        MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)));
+        col_dev = ctx->colout.as<int32_t>();
+    }
+    if (stats) memset(stats, 0, sizeof(*stats));
+    MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
+                           env_int("MUX_THETA", 6), env_int("MUX_TAIL", 16)));
+    if (out_on_host && n > 0) {
+        MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return MUX_OK;
+}
+
+int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, const double* share_host,
+              int64_t n, const double* y_host, int64_t m, int qbits, int32_t* col_of_row_host,
+              int64_t* total_q, mux_stats_t* stats, void* stream) {
+    if (!ctx) { set_error("null context"); return MUX_EINVAL; }
+    MUX_TRY(mux_table_validate(table));
+    if (n < 0 || m < 0) { set_error("mux_round: bad shape"); return MUX_EINVAL; }
+    if (qbits < 1 || qbits > 30) { set_error("mux_round: qbits must be in [1, 30]"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (total_q) *total_q = 0;
+    if (n == 0) return MUX_OK;
+    // H2D of the feature arrays through pinned staging (2n + m doubles)
+    const size_t fbytes = sizeof(double) * (size_t)(2 * n + m);
+    MUX_TRY(pinned_ensure(ctx, fbytes));
+    double* hp = static_cast<double*>(ctx->pinned);
+    memcpy(hp, x_host, sizeof(double) * n);
+    memcpy(hp + n, share_host, sizeof(double) * n);
+    if (m) memcpy(hp + 2 * n, y_host, sizeof(double) * m);
+    MUX_TRY(ctx->feat_in.ensure(fbytes));
+    double* dfeat = ctx->feat_in.as<double>();
+    MUX_CUDA_TRY(cudaMemcpyAsync(dfeat, hp, fbytes, cudaMemcpyHostToDevice, st));
+    const int64_t ldw = ((m + 3) / 4) * 4;
+    MUX_TRY(ctx->wq.ensure(sizeof(int32_t) * (size_t)n * (size_t)(ldw > 0 ? ldw : 4)));
+    cudaEvent_t e0, e1;
+    MUX_CUDA_TRY(cudaEventCreate(&e0));
+    MUX_CUDA_TRY(cudaEventCreate(&e1));
+    MUX_CUDA_TRY(cudaEventRecord(e0, st));
+    int64_t launches = 0;
+    if (m > 0)
+        MUX_TRY(mux_score_table_impl(ctx, table, dfeat, dfeat + n, n, dfeat + 2 * n, m, MUX_SCORE_EXACT,
+                                     MUX_W_I32, qbits, ctx->wq.ptr, ldw, st, &launches));
+    MUX_CUDA_TRY(cudaEventRecord(e1, st));
+    MUX_TRY(check_flags(ctx, st));
+    float ms_score = 0.f;
+    cudaEventElapsedTime(&ms_score, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)n));
+    int32_t* col_dev = ctx->colout.as<int32_t>();
+    MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, MUX_W_I32, n, m, ldw, col_dev, total_q, stats, st,
+                           env_int("MUX_THETA", 6), env_int("MUX_TAIL", 16)));
+    MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_host, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    if (stats) {
+        stats->ms_score = ms_score;
+        stats->launches += launches;
+    }
+    return MUX_OK;
+}
+
+}  // extern "C"
