@@ -295,7 +295,7 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": None, "algorithmic_bytes": auc_bytes, "kernel_ms": auc_ms},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": int(s["launches"]) + 3,
-        "solver": {k: s[k] for k in ("phases", "rounds", "bids", "row_scans", "tail_bids", "total_q")},
+        "solver": {k: s[k] for k in ("phases", "rounds", "bids", "row_scans", "tail_bids", "cache_hits", "total_q", "ms_tail", "ms_kernel")},
         "ms_match": auc_ms, "ms_per_step_all": times,
     }
     print(json.dumps(line), flush=True)

@@ -58,6 +58,26 @@ typedef struct {
     const double* values;
 } mux_table_t;
 
+/* MLP speed-predictor plugin weights (paper's predictor; no
+ * reference counterpart).  Network in(9) -> 64 -> 64 -> 64 -> 1 with ReLU,
+ * output clamped to [0, 1]; features are scaled (x - shift) * scale and
+ * ordered [online(4), offline(4), share], each workload contributing
+ * (gpu_utilization, sm_activity, sm_occupancy, iter_time_separate).
+ * Weight matrices are row-major [out][in].  Host pointers. */
+typedef struct {
+    const float* W1;     /* [64][9]  */
+    const float* b1;     /* [64]     */
+    const float* W2;     /* [64][64] */
+    const float* b2;     /* [64]     */
+    const float* W3;     /* [64][64] */
+    const float* b3;     /* [64]     */
+    const float* w4;     /* [64]     */
+    const float* shift;  /* [9]      */
+    const float* scale;  /* [9]      */
+    float b4;
+    int32_t hidden;      /* must be 64 */
+} mux_mlp_t;
+
 /* Per-solve statistics (filled by mux_match / mux_round when non-NULL). */
 typedef struct {
     int64_t n_rows;          /* N (real online rows)                      */
@@ -72,6 +92,9 @@ typedef struct {
     double  ms_score;        /* device time of the scoring kernel(s)       */
     double  ms_match;        /* device time of the auction                 */
     int64_t launches;        /* kernel launches issued by the call         */
+    double  ms_tail;         /* device time in single-CTA tail mode        */
+    double  ms_kernel;       /* device time of the auction kernel (globaltimer) */
+    int64_t cache_hits;      /* bids served from the candidate cache       */
 } mux_stats_t;
 
 typedef struct mux_ctx mux_ctx_t;
@@ -104,6 +127,18 @@ int mux_score_table(mux_ctx_t* ctx, const mux_table_t* table,
                     const double* y_dev, int64_t m,
                     int mode, int wtype, int qbits,
                     void* out_dev, int64_t ldo, void* stream);
+
+/*
+ * MLP pair scoring: the batched N x M evaluation of the MLP plugin, layers
+ * 2-3 as tcgen05 bf16 GEMMs with fp32 TMEM accumulation and fused
+ * bias/ReLU/dot epilogues.  on_dev: float64 [n][4], share_dev: float64 [n],
+ * off_dev: float64 [m][4] (DEVICE).  out_dev: [n][ldo] of MUX_W_F32 (scores)
+ * or MUX_W_I32 (rint(w * 2^qbits) after the 1e-6 edge floor), ldo % 4 == 0.
+ */
+int mux_score_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp,
+                  const double* on_dev, const double* share_dev, int64_t n,
+                  const double* off_dev, int64_t m, int wtype, int qbits,
+                  void* out_dev, int64_t ldo, void* stream);
 
 /*
  * Maximum-weight bipartite matching on non-negative integer weights

@@ -19,7 +19,7 @@ MUX_SCORE_EXACT, MUX_SCORE_FAST = 0, 1
 
 # every symbol include/muxflow.h declares (checked by tests/test_native_abi.py)
 EXPORTS = ("mux_version", "mux_last_error", "mux_ctx_create", "mux_ctx_destroy",
-           "mux_table_validate", "mux_score_table", "mux_match", "mux_round")
+           "mux_table_validate", "mux_score_table", "mux_score_mlp", "mux_match", "mux_round")
 
 
 class MuxTable(ctypes.Structure):
@@ -36,7 +36,8 @@ class MuxStats(ctypes.Structure):
                 ("n_rows", "n_cols", "n_square", "phases", "rounds", "bids", "row_scans",
                  "tail_bids", "total_q")] + \
                [("ms_score", ctypes.c_double), ("ms_match", ctypes.c_double),
-                ("launches", ctypes.c_int64)]
+                ("launches", ctypes.c_int64), ("ms_tail", ctypes.c_double),
+                ("ms_kernel", ctypes.c_double), ("cache_hits", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -75,6 +76,7 @@ def load():
         lib.mux_table_validate.argtypes = [ctypes.POINTER(MuxTable)]
         lib.mux_score_table.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int,
                                         ctypes.c_int, ctypes.c_int, P, i64, P]
+        lib.mux_score_mlp.argtypes = [P, P, P, P, i64, P, i64, ctypes.c_int, ctypes.c_int, P, i64, P]
         lib.mux_match.argtypes = [P, P, ctypes.c_int, i64, i64, i64, P, ctypes.c_int,
                                   ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         lib.mux_round.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int, P,

@@ -9,6 +9,9 @@
 int mux_score_table_impl(mux_ctx_t* ctx, const mux_table_t* tb, const double* x, const double* s,
                          int64_t n, const double* y, int64_t m, int mode, int wtype, int qbits,
                          void* out, int64_t ldo, cudaStream_t st, int64_t* launches);
+int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, const double* share, int64_t n,
+                       const double* off, int64_t m, int wtype, int qbits, void* out, int64_t ldo,
+                       cudaStream_t st, int64_t* launches);
 int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
                    int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
                    int theta, int tail_max);
@@ -78,7 +81,7 @@ int mux_ctx_destroy(mux_ctx_t* ctx) {
     if (!ctx) return MUX_OK;
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->table, &ctx->rowfeat, &ctx->colfeat, &ctx->flags, &ctx->feat_in, &ctx->wq,
-                      &ctx->colout, &ctx->auc})
+                      &ctx->colout, &ctx->auc, &ctx->mlp})
         b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
@@ -144,6 +147,21 @@ int mux_score_table(mux_ctx_t* ctx, const mux_table_t* table, const double* x_de
     int64_t launches = 0;
     MUX_TRY(mux_score_table_impl(ctx, table, x_dev, share_dev, n, y_dev, m, mode, wtype, qbits, out_dev, ldo, st, &launches));
     return check_flags(ctx, st);
+}
+
+int mux_score_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp, const double* on_dev, const double* share_dev,
+                  int64_t n, const double* off_dev, int64_t m, int wtype, int qbits, void* out_dev, int64_t ldo,
+                  void* stream) {
+    if (!ctx || !mlp) { set_error("null argument"); return MUX_EINVAL; }
+    if (n < 0 || m < 0 || ldo < m || (ldo % 4) != 0) { set_error("mux_score_mlp: bad shape"); return MUX_EINVAL; }
+    if (wtype != MUX_W_F32 && wtype != MUX_W_I32) { set_error("mux_score_mlp: output must be f32 or i32"); return MUX_EINVAL; }
+    if (wtype == MUX_W_I32 && (qbits < 0 || qbits > 30)) { set_error("qbits out of range"); return MUX_EINVAL; }
+    const float* ps[] = {mlp->W1, mlp->b1, mlp->W2, mlp->b2, mlp->W3, mlp->b3, mlp->w4, mlp->shift, mlp->scale};
+    for (const float* q : ps) if (!q) { set_error("mux_score_mlp: missing parameter"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    int64_t launches = 0;
+    return mux_score_mlp_impl(ctx, mlp, on_dev, share_dev, n, off_dev, m, wtype, qbits, out_dev, ldo,
+                              static_cast<cudaStream_t>(stream), &launches);
 }
 
 int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t m, int64_t ldw,

@@ -9,31 +9,35 @@
 // a_ij = Q_ij * (n + 1), so an assignment satisfying epsilon-complementary
 // slackness with epsilon = 1 is optimal (n * epsilon < n + 1 = one unit of Q).
 //
-// Algorithm (one persistent cooperative kernel for the whole solve):
+// One persistent cooperative kernel runs the whole solve (1 CTA per SM):
 //   for eps = eps0, eps0/theta, ..., 1:                  (epsilon scaling)
 //     clear the assignment, keep prices
 //     while some person is unassigned:
-//       if few remain: single-CTA Gauss-Seidel tail (no grid barriers)
+//       if <= tail_max remain: single-CTA Gauss-Seidel tail (no grid barriers)
 //       else Jacobi round:
-//         [A] every unassigned person computes its bid -- best object j1,
-//             best value v1, second value v2 (v = a - p), bid = p_j1 + v1 - v2 + eps
-//             -- from its top-K candidate cache when still valid, else from a
-//             full row scan (coalesced 16-byte loads of W and prices,
-//             per-lane top-(K+1) lists, warp-shuffle merge); the bid is
-//             atomicMax'ed into a packed 64-bit word (price << idbits | ~person)
-//         grid barrier
-//         [B] each bidder reads back the word: the winner takes the object,
-//             the previous owner and the losers form the next round's list
-//         grid barrier
-// Candidate cache: a full scan keeps the K best (object, benefit) pairs and the
-// (K+1)-th best value thr.  Prices only rise, so any uncached object's value
-// is still <= thr; if the best cached value is >= thr the cached top-2 (with
-// second = max(second, thr)) gives a valid epsilon-CS bid without re-reading
-// the row.  The cache stays valid across phases.
-// Determinism: every bid in a round sees the same prices and ties break to
-// the lowest object index / lowest person index, so results do not depend on
-// thread scheduling.
+//         [A1] each unassigned person bids from its top-K candidate cache
+//              (one warp per person); cache misses go to a global miss list
+//         [A2] misses are spread over the CTAs; each CTA scans one row at a
+//              time cooperatively: the weight row arrives by TMA bulk copy
+//              (cp.async.bulk, double-buffered) into shared memory, prices come
+//              from a shared-memory mirror, per-lane top-(K+1) lists are merged
+//              by warp shuffles, then across warps
+//         [B]  every bidder reads back the packed max-bid word of its object:
+//              the winner takes it, the previous owner and the losers form the
+//              next round's list
+// Values and objects travel as one 64-bit key (v + offset) << idbits | ~j, so
+// "largest key" = "best value, lowest object index on ties" and every
+// reduction is a plain unsigned max.  Bids are atomicMax'ed as
+// (price << idbits | ~person): highest bid wins, lowest person on ties.
+// Candidate cache: a scan keeps the K best (object, benefit) pairs and the
+// (K+1)-th best value thr.  Prices only rise, so uncached objects are still
+// worth <= thr; if the best cached value is >= thr the cached top-2 (second =
+// max(second, thr)) is a valid epsilon-CS bid without re-reading the row.
+// Determinism: all bids of a round see the same prices and every tie is
+// broken by index, so the result does not depend on thread scheduling.
 #include <cooperative_groups.h>
+
+#include <cstdio>
 
 #include "common.cuh"
 
@@ -44,24 +48,43 @@ namespace mux {
 constexpr int kK = 8;                 // cached candidates per person
 constexpr int kAucThreads = 512;      // 16 warps per CTA
 constexpr int kAucWarps = kAucThreads / kWarp;
-constexpr int kTailMax = 32;          // persons left when the single-CTA tail takes over
+constexpr int kTailMax = 64;          // largest tail handled by the single CTA
 constexpr int64_t kNegInf = INT64_MIN / 4;
+constexpr unsigned long long kNoKey = 0ull;
+constexpr size_t kSmemBudget = 220 * 1024;
+constexpr int kCandMax = 512;         // candidate keys kept by the threshold selection
 
 struct AucCounters {
     int32_t list_count[2];
     int32_t touched_count[2];
+    int32_t miss_count;
     uint32_t errors;
-    int32_t _pad;
-    unsigned long long rounds, bids, scans, tail_bids, phases;
+    uint32_t tail_epoch;
+    unsigned long long rounds, bids, scans, tail_bids, phases, hits;
+    long long ns_total, ns_tail, ns_tail_hit, ns_tail_scan, ns_tail_wait, ns_a1, ns_a2, ns_b;
+    unsigned long long tail_scans;
     long long max_q;
     long long total_q;
 };
+
+// Per-person candidate cache: one 128-byte record, read by a single lane
+// with seven 16-byte loads.
+struct __align__(128) PCache {
+    int32_t j[kK];       // cached objects, best first (-1 = empty)
+    int64_t q[kK];       // their weights (benefit = q * SC)
+    int64_t thr;         // (K+1)-th best value at scan time
+    int32_t valid;
+    int32_t pad[3];
+};
+static_assert(sizeof(PCache) == 128, "PCache must be one 128-byte line");
 
 struct AucArgs {
     const void* W;       // [N][ldw] int32 or int64
     int64_t ldw;
     int32_t N, M, n;     // real rows, real columns, square size
     int32_t idbits;
+    unsigned long long idmask;
+    int64_t koff;        // value offset making keys non-negative
     int64_t SC;          // benefit scale (n + 1)
     int64_t eps0;
     int32_t theta;
@@ -73,21 +96,70 @@ struct AucArgs {
     unsigned long long* bidw;   // [2][n_pad]
     int32_t* touched;    // [2][n_pad]
     int32_t* list;       // [2][n_pad]
+    int32_t* miss;       // [n_pad]
     int32_t* bidj;       // [n_pad]
     unsigned long long* bidpk;  // [n_pad]
-    int32_t* cj;         // [n_pad][K]
-    int64_t* ca;         // [n_pad][K]
-    int64_t* cthr;       // [n_pad]
-    int32_t* cvalid;     // [n_pad]
+    PCache* cache;       // [n_pad]
     AucCounters* cnt;
     int32_t n_pad;
+    int32_t row_bytes;   // bytes of one staged weight row (multiple of 16)
 };
 
-// ---- small helpers --------------------------------------------------------
+// ---- keys -------------------------------------------------------------------
 
-__device__ __forceinline__ bool better(int64_t v, int32_t j, int64_t bv, int32_t bj) {
-    return v > bv || (v == bv && j < bj);
+__device__ __forceinline__ unsigned long long mkkey(const AucArgs& A, int64_t v, int32_t j) {
+    return ((unsigned long long)(v + A.koff) << A.idbits) | (A.idmask - (unsigned long long)j);
 }
+__device__ __forceinline__ int32_t key_j(const AucArgs& A, unsigned long long k) {
+    return (int32_t)(A.idmask - (k & A.idmask));
+}
+__device__ __forceinline__ int64_t key_v(const AucArgs& A, unsigned long long k) {
+    return (int64_t)(k >> A.idbits) - A.koff;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(0xffffffffu, k, o);
+        k = x > k ? x : k;
+    }
+    return k;
+}
+
+// Lane-local sorted top-(K+1) keys, best first.
+struct TopKeys {
+    unsigned long long k[kK + 1];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int t = 0; t <= kK; ++t) k[t] = kNoKey;
+    }
+    __device__ __forceinline__ void push(unsigned long long x) {
+        if (x <= k[kK]) return;
+        k[kK] = x;
+#pragma unroll
+        for (int t = kK; t > 0; --t)
+            if (k[t] > k[t - 1]) { unsigned long long s = k[t]; k[t] = k[t - 1]; k[t - 1] = s; }
+    }
+    __device__ __forceinline__ void pop() {
+#pragma unroll
+        for (int t = 0; t < kK; ++t) k[t] = k[t + 1];
+        k[kK] = kNoKey;
+    }
+};
+
+// Merge the 32 lane lists; lane r (< K+1) receives the r-th best key.
+__device__ __forceinline__ unsigned long long warp_merge(TopKeys& L, int lane) {
+    unsigned long long mine = kNoKey;
+#pragma unroll 1
+    for (int r = 0; r <= kK; ++r) {
+        const unsigned long long b = warp_max_u64(L.k[0]);
+        if (b != kNoKey && L.k[0] == b) L.pop();
+        if (lane == r) mine = b;
+    }
+    return mine;
+}
+
+// ---- weights -----------------------------------------------------------------
 
 template <int WT>
 __device__ __forceinline__ int64_t wload1(const AucArgs& A, int32_t i, int32_t j) {
@@ -96,16 +168,26 @@ __device__ __forceinline__ int64_t wload1(const AucArgs& A, int32_t i, int32_t j
     return __ldg(static_cast<const int64_t*>(A.W) + (int64_t)i * A.ldw + j);
 }
 
-// Load 4 consecutive weights W[i][c..c+3] (c % 4 == 0), zero outside [0,N)x[0,M).
+// 4 consecutive weights of row i starting at column c (c % 4 == 0), read from
+// `row` (shared-memory copy of the row, may be null = global), zero outside
+// [0, N) x [0, M).
 template <int WT>
-__device__ __forceinline__ void wload4(const AucArgs& A, int32_t i, int32_t c, int64_t (&q)[4]) {
+__device__ __forceinline__ void wget4(const AucArgs& A, const void* row, int32_t i, int32_t c, int64_t (&q)[4]) {
     if (i >= A.N || c >= A.M) { q[0] = q[1] = q[2] = q[3] = 0; return; }
     if (WT == MUX_W_I32) {
-        const int4 v = __ldg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(A.W) + (int64_t)i * A.ldw + c));
+        int4 v;
+        if (row) v = reinterpret_cast<const int4*>(row)[c >> 2];
+        else v = __ldg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(A.W) + (int64_t)i * A.ldw + c));
         q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
     } else {
-        const longlong2* p = reinterpret_cast<const longlong2*>(static_cast<const int64_t*>(A.W) + (int64_t)i * A.ldw + c);
-        const longlong2 a = __ldg(p), b = __ldg(p + 1);
+        longlong2 a, b;
+        if (row) {
+            const longlong2* p = reinterpret_cast<const longlong2*>(row) + (c >> 1);
+            a = p[0]; b = p[1];
+        } else {
+            const longlong2* p = reinterpret_cast<const longlong2*>(static_cast<const int64_t*>(A.W) + (int64_t)i * A.ldw + c);
+            a = __ldg(p); b = __ldg(p + 1);
+        }
         q[0] = a.x; q[1] = a.y; q[2] = b.x; q[3] = b.y;
     }
     if (c + 4 > A.M) {
@@ -114,267 +196,427 @@ __device__ __forceinline__ void wload4(const AucArgs& A, int32_t i, int32_t c, i
     }
 }
 
-// Lane-local sorted top-(K+1) list, best first; equal values keep the earlier
-// (lower-index) object first because a lane visits its columns in ascending order.
-struct TopList {
-    int64_t v[kK + 1];
-    int32_t j[kK + 1];
-    __device__ __forceinline__ void init() {
-#pragma unroll
-        for (int k = 0; k <= kK; ++k) { v[k] = kNegInf; j[k] = INT32_MAX; }
-    }
-    __device__ __forceinline__ void push(int64_t nv, int32_t nj) {
-        if (!(nv > v[kK])) return;
-        v[kK] = nv; j[kK] = nj;
-#pragma unroll
-        for (int k = kK; k > 0; --k) {
-            if (v[k] > v[k - 1]) {
-                int64_t tv = v[k]; v[k] = v[k - 1]; v[k - 1] = tv;
-                int32_t tj = j[k]; j[k] = j[k - 1]; j[k - 1] = tj;
-            }
-        }
-    }
-    __device__ __forceinline__ void pop() {
-#pragma unroll
-        for (int k = 0; k < kK; ++k) { v[k] = v[k + 1]; j[k] = j[k + 1]; }
-        v[kK] = kNegInf; j[kK] = INT32_MAX;
-    }
+// ---- prices -------------------------------------------------------------------
+
+template <bool SP>
+__device__ __forceinline__ int64_t pget(const int64_t* P, int32_t j) { return SP ? P[j] : __ldcg(P + j); }
+
+template <bool SP>
+__device__ __forceinline__ void pget4(const int64_t* P, int32_t c, int64_t (&p)[4]) {
+    const longlong2* pp = reinterpret_cast<const longlong2*>(P + c);
+    longlong2 a, b;
+    if (SP) { a = pp[0]; b = pp[1]; }
+    else { a = __ldcg(pp); b = __ldcg(pp + 1); }
+    p[0] = a.x; p[1] = a.y; p[2] = b.x; p[3] = b.y;
+}
+
+// ---- TMA bulk copy + mbarrier -------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Arm the barrier for `bytes` and issue one bulk global->shared copy (thread 0).
+__device__ __forceinline__ void tma_row(uint64_t* bar, void* dst, const void* src, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+    // weight rows are streamed: evict them first so prices and caches stay in L2
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---- per-CTA shared state ------------------------------------------------------
+
+struct Shared {
+    uint64_t bar[2];                         // row-buffer mbarriers
+    uint32_t bar_phase[2];
+    int32_t row_person[2];                   // person whose row sits in buffer b (-1 none)
+    int32_t stack[kTailMax + 1];
+    int32_t top;
+    int32_t scan_i;                          // tail: person needing a scan (-1 = done)
+    int32_t j1;
+    int64_t bid;
+    unsigned long long wk[kAucWarps][kK + 1];  // per-warp merged keys (slow path)
+    unsigned long long wmax[kAucWarps];        // per-warp maximum key
+    unsigned long long tau;                    // selection threshold
+    unsigned long long sel[kK + 1];            // selected top-(K+1) keys
+    int32_t ncand;
+    unsigned long long cand[kCandMax];          // keys >= tau
 };
 
-// Warp argmax of (v, j) with ties to the lower j; result broadcast to all lanes.
-__device__ __forceinline__ void warp_argmax(int64_t& v, int32_t& j) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        int64_t ov = __shfl_xor_sync(0xffffffffu, v, o);
-        int32_t oj = __shfl_xor_sync(0xffffffffu, j, o);
-        if (better(ov, oj, v, j)) { v = ov; j = oj; }
-    }
+struct Dyn {             // carve-up of dynamic shared memory
+    int64_t* price;      // [n_pad] price mirror (SP mode)
+    int32_t* owner;      // [n_pad] owner mirror (SP mode, tail only)
+    unsigned char* row[2];
+};
+
+// Stage the price array (and owners) from global into the CTA's mirror.
+__device__ __forceinline__ void stage_prices(const AucArgs& A, int64_t* sp, int32_t* so) {
+    const longlong2* g = reinterpret_cast<const longlong2*>(A.price);
+    longlong2* s = reinterpret_cast<longlong2*>(sp);
+    for (int t = threadIdx.x; t < A.n_pad / 2; t += blockDim.x) s[t] = __ldcg(g + t);
+    if (so)
+        for (int t = threadIdx.x; t < A.n_pad; t += blockDim.x) so[t] = __ldcg(A.owner + t);
 }
 
-// Merge the 32 lane lists into the warp's top-(K+1).  Lane r (< K+1) ends up
-// holding the r-th best in (mv, mj).
-__device__ __forceinline__ void warp_merge(TopList& L, int lane, int64_t& mv, int32_t& mj) {
-    mv = kNegInf; mj = INT32_MAX;
-#pragma unroll 1
-    for (int r = 0; r <= kK; ++r) {
-        int64_t bv = L.v[0];
-        int32_t bj = L.j[0];
-        warp_argmax(bv, bj);
-        if (L.j[0] == bj && L.v[0] == bv && bj != INT32_MAX) L.pop();
-        if (lane == r) { mv = bv; mj = bj; }
-    }
+// Start fetching person i's weight row into buffer b (thread 0 only).
+__device__ __forceinline__ void drain_row(const AucArgs& A, Shared& S, int b) {
+    const int32_t p = S.row_person[b];
+    if (p >= 0 && p < A.N && A.M > 0) { mbar_wait(&S.bar[b], S.bar_phase[b]); S.bar_phase[b] ^= 1u; }
+    S.row_person[b] = -1;
 }
 
-// Scan the person's full row over objects [c_begin, n) with stride `stride`
-// columns per step (each lane handles 4 consecutive objects per step).
 template <int WT>
-__device__ __forceinline__ void scan_row(const AucArgs& A, int32_t i, int32_t c_begin, int32_t stride,
-                                         TopList& L) {
-    for (int32_t c = c_begin; c < A.n; c += stride) {
-        int64_t q[4];
-        wload4<WT>(A, i, c, q);
-        const longlong2* pp = reinterpret_cast<const longlong2*>(A.price + c);
-        const longlong2 p01 = __ldcg(pp), p23 = __ldcg(pp + 1);
-        const int64_t p[4] = {p01.x, p01.y, p23.x, p23.y};
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-            if (c + t < A.n) L.push(q[t] * A.SC - p[t], c + t);
-    }
+__device__ __forceinline__ void fetch_row(const AucArgs& A, Shared& S, Dyn& D, int b, int32_t i) {
+    drain_row(A, S, b);
+    S.row_person[b] = i;
+    if (i >= A.N || A.M == 0) return;            // dummy person: no weights to load
+    const size_t esz = WT == MUX_W_I32 ? 4 : 8;
+    const char* src = static_cast<const char*>(A.W) + (size_t)i * A.ldw * esz;
+    tma_row(&S.bar[b], D.row[b], src, (uint32_t)A.row_bytes);
 }
-
-// Store a fresh cache for person i from lane-held ranks (lane r holds rank r).
+// Wait for buffer b (all threads); returns the row pointer.
 template <int WT>
-__device__ __forceinline__ void store_cache(const AucArgs& A, int32_t i, int lane, int64_t mv, int32_t mj) {
-    if (lane < kK) {
-        const bool ok = mj != INT32_MAX;
-        A.cj[(int64_t)i * kK + lane] = ok ? mj : -1;
-        A.ca[(int64_t)i * kK + lane] = ok ? wload1<WT>(A, i, mj) * A.SC : 0;
-    }
-    const int64_t thr = __shfl_sync(0xffffffffu, mv, kK);
-    if (lane == 0) {
-        A.cthr[i] = thr;   // kNegInf when fewer than K+1 objects exist
-        A.cvalid[i] = 1;
-    }
+__device__ __forceinline__ const void* wait_row(const AucArgs& A, Shared& S, Dyn& D, int b, int32_t i) {
+    if (i >= A.N || A.M == 0) return D.row[b];
+    mbar_wait(&S.bar[b], S.bar_phase[b]);
+    return D.row[b];
 }
 
-// Bid from the candidate cache.  Returns true (and j1, bid) on a valid hit.
-__device__ __forceinline__ bool cache_bid(const AucArgs& A, int32_t i, int lane, int64_t eps,
+// ---- bids ----------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t bid_from(int64_t a1, int64_t v1, int64_t second, int64_t eps) {
+    return (second <= kNegInf) ? (a1 - v1) + eps : a1 - second + eps;   // n == 1: price + eps
+}
+
+// Bid from the candidate cache by ONE thread (no shuffles).  True on a valid
+// hit; ties on value go to the lower object index, like a full scan.
+template <bool SP>
+__device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, int32_t i, int64_t eps,
                                           int32_t& j1, int64_t& bid) {
-    if (!__ldcg(A.cvalid + i)) return false;
-    int64_t v = kNegInf, a = 0;
-    int32_t j = INT32_MAX;
-    if (lane < kK) {
-        const int32_t cj = __ldcg(A.cj + (int64_t)i * kK + lane);
-        if (cj >= 0) {
-            a = __ldcg(A.ca + (int64_t)i * kK + lane);
-            v = a - __ldcg(A.price + cj);
-            j = cj;
-        }
+    const longlong2* rec = reinterpret_cast<const longlong2*>(A.cache + i);
+    longlong2 w[7];      // j[0..8) | q[0..8) | thr, valid
+#pragma unroll
+    for (int t = 0; t < 7; ++t) w[t] = __ldcg(rec + t);
+    const int32_t valid = (int32_t)(w[6].y & 0xffffffffll);
+    if (!valid) return false;
+    const int64_t thr = w[6].x;
+    const int32_t* jj = reinterpret_cast<const int32_t*>(&w[0]);
+    const int64_t* qq = reinterpret_cast<const int64_t*>(&w[2]);
+    int64_t v1 = kNegInf, v2 = kNegInf, a1 = 0;
+    int32_t b = INT32_MAX;
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+        const int32_t j = jj[k];
+        if (j < 0) continue;
+        const int64_t a = qq[k] * A.SC;
+        const int64_t v = a - pget<SP>(P, j);
+        if (v > v1 || (v == v1 && j < b)) { v2 = v1; v1 = v; b = j; a1 = a; }
+        else if (v > v2) v2 = v;
     }
-    int64_t bv = v;
-    int32_t bj = j;
-    warp_argmax(bv, bj);
-    // second best: max over the other lanes
-    int64_t sv = (j == bj) ? kNegInf : v;
-    int32_t sj = (j == bj) ? INT32_MAX : j;
-    warp_argmax(sv, sj);
-    const int64_t thr = __ldcg(A.cthr + i);
-    if (bj == INT32_MAX || bv < thr) return false;
-    const int64_t second = sv > thr ? sv : thr;
-    const int64_t a1 = __shfl_sync(0xffffffffu, a, __ffs(__ballot_sync(0xffffffffu, j == bj)) - 1);
-    j1 = bj;
-    // a single object (n == 1): bid price + eps
-    bid = (second <= kNegInf) ? (a1 - bv) + eps : a1 - second + eps;
+    if (b == INT32_MAX || v1 < thr) return false;
+    const int64_t s2 = v2 > thr ? v2 : thr;
+    j1 = b;
+    bid = bid_from(a1, v1, s2, eps);
     return true;
 }
 
-// Full-row bid by one warp (bulk rounds).
-template <int WT>
-__device__ __forceinline__ void warp_scan_bid(const AucArgs& A, int32_t i, int lane, int64_t eps,
-                                              int32_t& j1, int64_t& bid) {
-    TopList L;
-    L.init();
-    scan_row<WT>(A, i, lane * 4, 32 * 4, L);
-    int64_t mv;
-    int32_t mj;
-    warp_merge(L, lane, mv, mj);
-    store_cache<WT>(A, i, lane, mv, mj);
-    const int64_t v1 = __shfl_sync(0xffffffffu, mv, 0);
-    const int32_t jj = __shfl_sync(0xffffffffu, mj, 0);
-    const int64_t v2 = __shfl_sync(0xffffffffu, mv, 1);
-    const int64_t a1 = wload1<WT>(A, i, jj) * A.SC;
-    j1 = jj;
-    bid = (v2 <= kNegInf) ? (a1 - v1) + eps : a1 - v2 + eps;
+// Key of row i at column c (4 consecutive), zero key for padding columns.
+template <int WT, bool SP>
+__device__ __forceinline__ void keys4(const AucArgs& A, const int64_t* P, const void* row, int32_t i, int32_t c,
+                                      unsigned long long (&k)[4]) {
+    int64_t q[4], p[4];
+    wget4<WT>(A, row, i, c, q);
+    pget4<SP>(P, c, p);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) k[t] = (c + t < A.n) ? mkkey(A, q[t] * A.SC - p[t], c + t) : kNoKey;
+}
+
+// Scan a row with the whole CTA: `row` is the staged weight row (or null =
+// read from global), P the price source.  Stores the new cache and leaves the
+// bid in S.j1 / S.bid (valid after the trailing barrier).
+//
+// Top-(K+1) selection without sorting networks: tau = the (K+1)-th largest of
+// the 16 per-warp maxima is a lower bound on the (K+1)-th largest key, so the
+// answer lies among the keys >= tau (typically ~K+1 of them); those are
+// collected in shared memory and ranked by direct comparison.  Rows shorter
+// than 16 x 128 columns, or degenerate candidate sets, take the shuffle-merge
+// path.
+template <int WT, bool SP>
+__device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, const void* row, int32_t i,
+                             int64_t eps) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool fast = A.n > (kK * 128);   // >= K+1 warps hold columns
+    bool done = false;
+    if (fast) {
+        unsigned long long mx = kNoKey;
+        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4) {
+            unsigned long long k[4];
+            keys4<WT, SP>(A, P, row, i, c, k);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) mx = k[t] > mx ? k[t] : mx;
+        }
+        mx = warp_max_u64(mx);
+        if (lane == 0) S.wmax[warp] = mx;
+        if (threadIdx.x == 0) S.ncand = 0;
+        __syncthreads();
+        if (warp == 0 && lane < kAucWarps) {
+            const unsigned long long v = S.wmax[lane];
+            int rank = 0;
+#pragma unroll
+            for (int w = 0; w < kAucWarps; ++w) {
+                const unsigned long long o = S.wmax[w];
+                rank += (o > v) || (o == v && w < lane);
+            }
+            if (rank == kK) S.tau = v;
+        }
+        __syncthreads();
+        const unsigned long long tau = S.tau;
+        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4) {
+            unsigned long long k[4];
+            keys4<WT, SP>(A, P, row, i, c, k);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (k[t] >= tau && k[t] != kNoKey) {
+                    const int slot = atomicAdd(&S.ncand, 1);
+                    if (slot < kCandMax) S.cand[slot] = k[t];
+                }
+        }
+        __syncthreads();
+        const int nc = S.ncand;
+        if (nc <= kCandMax) {
+            for (int t = threadIdx.x; t < nc; t += kAucThreads) {
+                const unsigned long long key = S.cand[t];
+                int rank = 0;
+                for (int e = 0; e < nc; ++e) rank += S.cand[e] > key;
+                if (rank <= kK) S.sel[rank] = key;
+            }
+            if (threadIdx.x <= kK && threadIdx.x >= nc) S.sel[threadIdx.x] = kNoKey;
+            done = true;
+        }
+    }
+    if (!done) {
+        TopKeys L;
+        L.init();
+        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4) {
+            unsigned long long k[4];
+            keys4<WT, SP>(A, P, row, i, c, k);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) L.push(k[t]);
+        }
+        const unsigned long long wk = warp_merge(L, lane);
+        if (lane <= kK) S.wk[warp][lane] = wk;
+        __syncthreads();
+        if (warp == 0) {
+            TopKeys M;
+            M.init();
+            for (int e = lane; e < kAucWarps * (kK + 1); e += 32) M.push(S.wk[e / (kK + 1)][e % (kK + 1)]);
+            const unsigned long long mk = warp_merge(M, lane);
+            if (lane <= kK) S.sel[lane] = mk;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // cache: lanes 0..K-1 hold ranks 0..K-1, rank K is the threshold
+        const unsigned long long mk = lane <= kK ? S.sel[lane] : kNoKey;
+        PCache* rec = A.cache + i;
+        if (lane < kK) {
+            const bool ok = mk != kNoKey;
+            const int32_t j = ok ? key_j(A, mk) : -1;
+            rec->j[lane] = j;
+            rec->q[lane] = ok ? (key_v(A, mk) + pget<SP>(P, j)) / A.SC : 0;
+        }
+        if (lane == 0) {
+            const unsigned long long k0 = S.sel[0], k1 = S.sel[1], kt = S.sel[kK];
+            rec->thr = kt == kNoKey ? kNegInf : key_v(A, kt);
+            rec->valid = 1;
+            const int32_t jj = key_j(A, k0);
+            const int64_t v1 = key_v(A, k0);
+            const int64_t a1 = v1 + pget<SP>(P, jj);
+            S.j1 = jj;
+            S.bid = bid_from(a1, v1, k1 == kNoKey ? kNegInf : key_v(A, k1), eps);
+        }
+    }
+    __syncthreads();
 }
 
 __device__ __forceinline__ unsigned long long pack_bid(const AucArgs& A, int64_t bid, int32_t i) {
-    const unsigned long long idmask = (1ull << A.idbits) - 1ull;
-    return ((unsigned long long)bid << A.idbits) | (idmask - (unsigned long long)i);
+    return ((unsigned long long)bid << A.idbits) | (A.idmask - (unsigned long long)i);
 }
 
-// ---- single-CTA Gauss-Seidel tail -----------------------------------------
+__device__ __forceinline__ void check_bid(const AucArgs& A, int64_t bid) {
+    if (bid < 0 || (unsigned long long)bid >= (1ull << (63 - A.idbits))) atomicOr(&A.cnt->errors, kErrPriceBits);
+}
 
-template <int WT>
-__device__ void tail_gs(const AucArgs& A, int64_t eps, int32_t count, const int32_t* src_list) {
-    __shared__ int32_t stack[kTailMax + 1];
-    __shared__ int32_t s_top;
-    __shared__ int64_t s_mv[kAucWarps][kK + 1];
-    __shared__ int32_t s_mj[kAucWarps][kK + 1];
-    __shared__ int32_t s_j1;
-    __shared__ int64_t s_bid;
-    __shared__ int32_t s_hit;
+__device__ __forceinline__ void submit_bid(const AucArgs& A, unsigned long long* bw, int32_t i, int32_t j1,
+                                           int64_t bid) {
+    const unsigned long long pk = pack_bid(A, bid, i);
+    check_bid(A, bid);
+    atomicMax(bw + j1, pk);
+    A.bidj[i] = j1;
+    A.bidpk[i] = pk;
+}
+
+// Gauss-Seidel assignment of object j1 to person i at price `bid` (tail mode,
+// thread 0).  Returns the displaced person or -1.
+template <bool SP>
+__device__ __forceinline__ int32_t gs_assign(const AucArgs& A, Dyn& D, int32_t i, int32_t j1, int64_t bid) {
+    check_bid(A, bid);
+    const int32_t prev = SP ? D.owner[j1] : __ldcg(A.owner + j1);
+    if (SP) { D.owner[j1] = i; D.price[j1] = bid; }
+    A.owner[j1] = i;
+    A.price[j1] = bid;
+    A.col[i] = j1;
+    if (prev >= 0) A.col[prev] = -1;
+    return prev;
+}
+
+// ---- single-CTA Gauss-Seidel tail -----------------------------------------------
+
+template <int WT, bool SP>
+__device__ void tail_gs(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_t count, const int32_t* src) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int t = threadIdx.x; t < count; t += blockDim.x) stack[t] = __ldcg(src_list + t);
+    if (SP) stage_prices(A, D.price, D.owner);
+    const int64_t* P = SP ? D.price : A.price;
+    for (int t = threadIdx.x; t < count; t += blockDim.x) S.stack[t] = __ldcg(src + t);
     __syncthreads();
     if (threadIdx.x == 0) {
-        // the list order comes from atomics; sort (descending, so the lowest
-        // person id is popped first) to keep the tail deterministic
+        // the list order comes from atomics: sort (descending) so the lowest
+        // person id is popped first and the tail is deterministic
         for (int a = 1; a < count; ++a) {
-            const int32_t key = stack[a];
+            const int32_t key = S.stack[a];
             int b = a - 1;
-            while (b >= 0 && stack[b] < key) { stack[b + 1] = stack[b]; --b; }
-            stack[b + 1] = key;
+            while (b >= 0 && S.stack[b] < key) { S.stack[b + 1] = S.stack[b]; --b; }
+            S.stack[b + 1] = key;
         }
-        s_top = count;
+        S.top = count;
     }
     __syncthreads();
-    unsigned long long steps = 0, scans = 0;
-    while (s_top > 0) {
-        const int32_t i = stack[s_top - 1];
-        if (warp == 0) {
-            int32_t j1;
-            int64_t bid;
-            const bool hit = cache_bid(A, i, lane, eps, j1, bid);
-            if (lane == 0) { s_hit = hit; s_j1 = j1; s_bid = bid; }
-        }
-        __syncthreads();
-        if (!s_hit) {
-            TopList L;
-            L.init();
-            scan_row<WT>(A, i, (warp * 32 + lane) * 4, kAucThreads * 4, L);
-            int64_t mv;
-            int32_t mj;
-            warp_merge(L, lane, mv, mj);
-            if (lane <= kK) { s_mv[warp][lane] = mv; s_mj[warp][lane] = mj; }
-            __syncthreads();
-            if (warp == 0) {
-                TopList M;
-                M.init();
-                // lane l takes candidates l, l+32, ... of the kAucWarps*(K+1) pool,
-                // pushed in ascending object order per lane is not guaranteed, so
-                // use the full (v, j) order explicitly.
-                for (int e = lane; e < kAucWarps * (kK + 1); e += 32) {
-                    const int64_t v = s_mv[e / (kK + 1)][e % (kK + 1)];
-                    const int32_t j = s_mj[e / (kK + 1)][e % (kK + 1)];
-                    if (j == INT32_MAX) continue;
-                    // insertion honouring ties by lower j
-                    if (better(v, j, M.v[kK], M.j[kK])) {
-                        M.v[kK] = v; M.j[kK] = j;
-#pragma unroll
-                        for (int k = kK; k > 0; --k)
-                            if (better(M.v[k], M.j[k], M.v[k - 1], M.j[k - 1])) {
-                                int64_t tv = M.v[k]; M.v[k] = M.v[k - 1]; M.v[k - 1] = tv;
-                                int32_t tj = M.j[k]; M.j[k] = M.j[k - 1]; M.j[k - 1] = tj;
-                            }
-                    }
-                }
-                warp_merge(M, lane, mv, mj);
-                store_cache<WT>(A, i, lane, mv, mj);
-                const int64_t v1 = __shfl_sync(0xffffffffu, mv, 0);
-                const int32_t jj = __shfl_sync(0xffffffffu, mj, 0);
-                const int64_t v2 = __shfl_sync(0xffffffffu, mv, 1);
-                if (lane == 0) {
-                    const int64_t a1 = wload1<WT>(A, i, jj) * A.SC;
-                    s_j1 = jj;
-                    s_bid = (v2 <= kNegInf) ? (a1 - v1) + eps : a1 - v2 + eps;
-                }
-            }
-            ++scans;
-        }
-        __syncthreads();
+    unsigned long long steps = 0, scans = 0, hits = 0;
+    uint64_t ns_hit = 0, ns_scan = 0, ns_wait = 0;
+    int cur_buf = 0;
+    for (;;) {
+        const uint64_t th0 = gtimer();
+        // warp 0 runs every cache-hit step alone (no CTA barrier); it stops at
+        // the first miss and hands that person to the whole CTA.
         if (threadIdx.x == 0) {
-            const int32_t j = s_j1;
-            const int64_t bid = s_bid;
-            const int32_t prev = A.owner[j];
-            A.owner[j] = i;
-            A.price[j] = bid;
-            A.col[i] = j;
-            --s_top;
-            if (prev >= 0) {
-                A.col[prev] = -1;
-                stack[s_top++] = prev;
+            int32_t need = -1;
+            int32_t top = S.top;
+            while (top > 0 && steps <= (unsigned long long)A.round_guard) {
+                const int32_t i = S.stack[top - 1];
+                int32_t j1 = 0;
+                int64_t bid = 0;
+                if (!cache_bid<SP>(A, P, i, eps, j1, bid)) { need = i; break; }
+                const int32_t prev = gs_assign<SP>(A, D, i, j1, bid);
+                --top;
+                if (prev >= 0) S.stack[top++] = prev;
+                ++hits;
+                ++steps;
             }
-            __threadfence_block();
+            S.top = top;
+            S.scan_i = steps > (unsigned long long)A.round_guard ? -2 : need;
+            if (need >= 0 && SP && S.row_person[cur_buf] != need) fetch_row<WT>(A, S, D, cur_buf, need);
         }
+        __syncthreads();
+        const uint64_t th1 = gtimer();
+        ns_hit += th1 - th0;
+        const int32_t i = S.scan_i;
+        if (i < 0) break;
+        const void* row = SP ? wait_row<WT>(A, S, D, cur_buf, i) : nullptr;
+        const uint64_t th2 = gtimer();
+        ns_wait += th2 - th1;
+        cta_scan_bid<WT, SP>(A, S, P, row, i, eps);
+        if (threadIdx.x == 0) {
+            if (SP && i < A.N && A.M > 0) S.bar_phase[cur_buf] ^= 1u;
+            S.row_person[cur_buf] = -1;
+            const int32_t prev = gs_assign<SP>(A, D, i, S.j1, S.bid);
+            int32_t t2 = S.top - 1;
+            if (prev >= 0) {
+                S.stack[t2++] = prev;
+                // prefetch the displaced person's row: it bids next
+                if (SP) fetch_row<WT>(A, S, D, cur_buf ^ 1, prev);
+            }
+            S.top = t2;
+        }
+        if (SP) cur_buf ^= 1;
+        ++scans;
         ++steps;
         __syncthreads();
-        if (steps > (unsigned long long)A.round_guard) {
-            if (threadIdx.x == 0) atomicOr(&A.cnt->errors, kErrIterGuard);
-            break;
-        }
+        ns_scan += gtimer() - th1;
     }
+    if (S.scan_i == -2 && threadIdx.x == 0) atomicOr(&A.cnt->errors, kErrIterGuard);
+    // drain a pending prefetch so the mbarrier phases stay consistent
+    if (SP && threadIdx.x == 0) { drain_row(A, S, 0); drain_row(A, S, 1); }
     if (threadIdx.x == 0) {
         atomicAdd(&A.cnt->tail_bids, steps);
         atomicAdd(&A.cnt->bids, steps);
         atomicAdd(&A.cnt->scans, scans);
+        atomicAdd(&A.cnt->hits, hits);
+        atomicAdd(&A.cnt->tail_scans, scans);
+        atomicAdd((unsigned long long*)&A.cnt->ns_tail_hit, (unsigned long long)ns_hit);
+        atomicAdd((unsigned long long*)&A.cnt->ns_tail_scan, (unsigned long long)ns_scan);
+        atomicAdd((unsigned long long*)&A.cnt->ns_tail_wait, (unsigned long long)ns_wait);
         __threadfence();
     }
+    __syncthreads();
 }
 
-// ---- the persistent solve kernel ------------------------------------------
+// ---- the persistent solve kernel --------------------------------------------------
 
-template <int WT>
-__global__ void __launch_bounds__(kAucThreads)
+template <int WT, bool SP>
+__global__ void __launch_bounds__(kAucThreads, 1)
 auction_kernel(AucArgs A) {
     cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ Shared S;
+    Dyn D;
+    {
+        unsigned char* p = dsm;
+        D.row[0] = p; p += A.row_bytes;
+        D.row[1] = p; p += A.row_bytes;
+        D.price = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * A.n_pad;
+        D.owner = reinterpret_cast<int32_t*>(p);
+    }
     const int lane = threadIdx.x & 31;
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
-    const int64_t gwarp = gtid >> 5;
-    const int64_t nwarps = gsize >> 5;
     const int n = A.n;
+    if (threadIdx.x == 0) {
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 1);
+        fence_mbar_init();
+        S.bar_phase[0] = S.bar_phase[1] = 0;
+        S.row_person[0] = S.row_person[1] = -1;
+    }
+    __syncthreads();
     int64_t eps = A.eps0;
     long long rounds_total = 0;
+    uint32_t tail_epoch = 0;
+    uint64_t t_a1 = 0, t_a2 = 0, t_b = 0;
+    const uint64_t t_start = gtimer();
+    uint64_t t_tail = 0;
 
     for (;;) {
         // ---- phase init: clear the assignment, keep prices and caches
@@ -390,6 +632,7 @@ auction_kernel(AucArgs A) {
             A.cnt->list_count[1] = 0;
             A.cnt->touched_count[0] = 0;
             A.cnt->touched_count[1] = 0;
+            A.cnt->miss_count = 0;
             atomicAdd(&A.cnt->phases, 1ull);
         }
         grid.sync();
@@ -399,53 +642,99 @@ auction_kernel(AucArgs A) {
             const int32_t count = __ldcg(&A.cnt->list_count[cur]);
             if (count == 0) break;
             if (count <= A.tail_max) {
+                ++tail_epoch;
                 if (blockIdx.x == 0) {
-                    if (WT == MUX_W_I32) tail_gs<MUX_W_I32>(A, eps, count, A.list + (int64_t)cur * A.n_pad);
-                    else tail_gs<MUX_W_I64>(A, eps, count, A.list + (int64_t)cur * A.n_pad);
+                    const uint64_t t0 = gtimer();
+                    tail_gs<WT, SP>(A, S, D, eps, count, A.list + (int64_t)cur * A.n_pad);
+                    t_tail += gtimer() - t0;
+                    if (threadIdx.x == 0) {
+                        __threadfence();
+                        atomicExch(&A.cnt->tail_epoch, tail_epoch);
+                    }
+                } else if (threadIdx.x == 0) {
+                    // idle CTAs sleep instead of polling a grid barrier, so the
+                    // single working CTA keeps the L2 to itself
+                    unsigned ns = 256;
+                    while (*reinterpret_cast<volatile uint32_t*>(&A.cnt->tail_epoch) != tail_epoch) {
+                        __nanosleep(ns);
+                        ns = ns < 16384 ? ns * 2 : ns;
+                    }
+                    __threadfence();
                 }
                 grid.sync();
                 break;
             }
-            // ---- [A] bids
+            const int32_t* L = A.list + (int64_t)cur * A.n_pad;
+            unsigned long long* bw = A.bidw + (int64_t)cur * A.n_pad;
+            const uint64_t tr0 = gtimer();
+            // ---- [A1] cache bids (warp per person), misses to the global list
             {
                 const int32_t tcount = __ldcg(&A.cnt->touched_count[nxt]);
                 const int32_t* tl = A.touched + (int64_t)nxt * A.n_pad;
                 unsigned long long* bw_old = A.bidw + (int64_t)nxt * A.n_pad;
                 for (int64_t t = gtid; t < tcount; t += gsize) bw_old[__ldcg(tl + t)] = 0ull;
                 if (gtid == 0) A.cnt->list_count[nxt] = 0;
-            }
-            unsigned long long my_scans = 0;
-            {
-                const int32_t* L = A.list + (int64_t)cur * A.n_pad;
-                unsigned long long* bw = A.bidw + (int64_t)cur * A.n_pad;
-                for (int64_t idx = gwarp; idx < count; idx += nwarps) {
+                unsigned long long my_hits = 0;
+                for (int64_t idx = gtid; idx < count; idx += gsize) {
                     const int32_t i = __ldcg(L + idx);
-                    int32_t j1;
-                    int64_t bid;
-                    if (!cache_bid(A, i, lane, eps, j1, bid)) {
-                        warp_scan_bid<WT>(A, i, lane, eps, j1, bid);
-                        ++my_scans;
+                    int32_t j1 = 0;
+                    int64_t bid = 0;
+                    if (cache_bid<false>(A, A.price, i, eps, j1, bid)) {
+                        submit_bid(A, bw, i, j1, bid);
+                        ++my_hits;
+                    } else {
+                        A.miss[atomicAdd(&A.cnt->miss_count, 1)] = i;
                     }
-                    if (lane == 0) {
-                        const unsigned long long pk = pack_bid(A, bid, i);
-                        if (bid < 0 || (unsigned long long)bid >= (1ull << (63 - A.idbits)))
-                            atomicOr(&A.cnt->errors, kErrPriceBits);
-                        atomicMax(bw + j1, pk);
-                        A.bidj[i] = j1;
-                        A.bidpk[i] = pk;
+                }
+                my_hits += __shfl_xor_sync(0xffffffffu, my_hits, 16);
+                my_hits += __shfl_xor_sync(0xffffffffu, my_hits, 8);
+                my_hits += __shfl_xor_sync(0xffffffffu, my_hits, 4);
+                my_hits += __shfl_xor_sync(0xffffffffu, my_hits, 2);
+                my_hits += __shfl_xor_sync(0xffffffffu, my_hits, 1);
+                if (lane == 0 && my_hits) atomicAdd(&A.cnt->hits, my_hits);
+            }
+            grid.sync();
+            const uint64_t tr1 = gtimer();
+            // ---- [A2] cooperative row scans for the misses, spread over CTAs
+            {
+                const int32_t nmiss = __ldcg(&A.cnt->miss_count);
+                if ((int32_t)blockIdx.x < nmiss) {
+                    if (SP) {
+                        if (threadIdx.x == 0) fetch_row<WT>(A, S, D, 0, __ldcg(A.miss + blockIdx.x));
+                        stage_prices(A, D.price, nullptr);
+                        __syncthreads();
+                    }
+                    int b = 0;
+                    for (int32_t e = blockIdx.x; e < nmiss; e += gridDim.x) {
+                        const int32_t i = __ldcg(A.miss + e);
+                        const void* row = SP ? wait_row<WT>(A, S, D, b, i) : nullptr;
+                        // prefetch the next miss into the other buffer
+                        if (SP && threadIdx.x == 0 && e + (int32_t)gridDim.x < nmiss)
+                            fetch_row<WT>(A, S, D, b ^ 1, __ldcg(A.miss + e + gridDim.x));
+                        cta_scan_bid<WT, SP>(A, S, SP ? D.price : A.price, row, i, eps);
+                        if (threadIdx.x == 0) {
+                            submit_bid(A, bw, i, S.j1, S.bid);
+                            if (SP && i < A.N && A.M > 0) S.bar_phase[b] ^= 1u;
+                            S.row_person[b] = -1;
+                        }
+                        b ^= 1;
+                        __syncthreads();
+                    }
+                    if (threadIdx.x == 0) {
+                        const int32_t my = (nmiss - (int32_t)blockIdx.x + (int32_t)gridDim.x - 1) / (int32_t)gridDim.x;
+                        atomicAdd(&A.cnt->scans, (unsigned long long)my);
                     }
                 }
             }
-            if (lane == 0 && my_scans) atomicAdd(&A.cnt->scans, my_scans);
             grid.sync();
+            const uint64_t tr2 = gtimer();
             // ---- [B] resolve
             {
-                const int32_t* L = A.list + (int64_t)cur * A.n_pad;
                 int32_t* Lnext = A.list + (int64_t)nxt * A.n_pad;
-                const unsigned long long* bw = A.bidw + (int64_t)cur * A.n_pad;
                 int32_t* tl = A.touched + (int64_t)cur * A.n_pad;
                 if (gtid == 0) {
                     A.cnt->touched_count[nxt] = 0;
+                    A.cnt->miss_count = 0;
                     atomicAdd(&A.cnt->rounds, 1ull);
                     atomicAdd(&A.cnt->bids, (unsigned long long)count);
                 }
@@ -469,6 +758,12 @@ auction_kernel(AucArgs A) {
                 }
             }
             grid.sync();
+            if (gtid == 0) {
+                const uint64_t tr3 = gtimer();
+                t_a1 += tr1 - tr0;
+                t_a2 += tr2 - tr1;
+                t_b += tr3 - tr2;
+            }
             ++r;
             if (++rounds_total > A.round_guard) {
                 if (gtid == 0) atomicOr(&A.cnt->errors, kErrIterGuard);
@@ -479,6 +774,13 @@ auction_kernel(AucArgs A) {
         if (eps <= 1) break;
         eps = eps / A.theta;
         if (eps < 1) eps = 1;
+    }
+    if (gtid == 0) {
+        A.cnt->ns_total = (long long)(gtimer() - t_start);
+        A.cnt->ns_tail = (long long)t_tail;
+        A.cnt->ns_a1 = (long long)t_a1;
+        A.cnt->ns_a2 = (long long)t_a2;
+        A.cnt->ns_b = (long long)t_b;
     }
 }
 
@@ -537,9 +839,9 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     if (wtype != MUX_W_I32 && wtype != MUX_W_I64) { set_error("mux_match: weights must be int32 or int64"); return MUX_EINVAL; }
     const int64_t n = N > M ? N : M;
     if (n >= (1ll << 30)) { set_error("mux_match: problem too large"); return MUX_EINVAL; }
+    const int esz = wtype == MUX_W_I32 ? 4 : 8;
     if (N > 0 && M > 0) {
-        const int vec = wtype == MUX_W_I32 ? 4 : 2;
-        if ((ldw % vec) != 0 || (reinterpret_cast<uintptr_t>(W) & 15) != 0) {
+        if (((ldw * esz) % 16) != 0 || (reinterpret_cast<uintptr_t>(W) & 15) != 0) {
             set_error("mux_match: rows must be 16-byte aligned (ldw multiple of 16 bytes)");
             return MUX_EINVAL;
         }
@@ -547,7 +849,10 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     if (total_q) *total_q = 0;
     if (n == 0) return MUX_OK;
     const int32_t n_pad = (int32_t)(((n + 3) / 4) * 4 + 4);
-    // workspace layout
+    // a staged row covers columns [0, M) rounded up to 16 bytes (<= ldw)
+    int64_t row_cols = ((M + 3) / 4) * 4;
+    if (row_cols > ldw) row_cols = ldw;
+    const int32_t row_bytes = (int32_t)(row_cols * esz);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
     const size_t o_cnt = take(sizeof(AucCounters));
@@ -557,16 +862,15 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     const size_t o_bidw = take(16ull * n_pad);
     const size_t o_touch = take(8ull * n_pad);
     const size_t o_list = take(8ull * n_pad);
+    const size_t o_miss = take(4ull * n_pad);
     const size_t o_bidj = take(4ull * n_pad);
     const size_t o_bidpk = take(8ull * n_pad);
-    const size_t o_cj = take(4ull * kK * n_pad);
-    const size_t o_ca = take(8ull * kK * n_pad);
-    const size_t o_cthr = take(8ull * n_pad);
-    const size_t o_cvalid = take(4ull * n_pad);
+    const size_t o_cache = take(sizeof(PCache) * (size_t)n_pad);
     MUX_TRY(ctx->auc.ensure(off));
     char* base = ctx->auc.as<char>();
     AucArgs A;
     A.W = W; A.ldw = ldw; A.N = (int32_t)N; A.M = (int32_t)M; A.n = (int32_t)n; A.n_pad = n_pad;
+    A.row_bytes = row_bytes;
     A.cnt = reinterpret_cast<AucCounters*>(base + o_cnt);
     A.price = reinterpret_cast<int64_t*>(base + o_price);
     A.owner = reinterpret_cast<int32_t*>(base + o_owner);
@@ -574,21 +878,21 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.bidw = reinterpret_cast<unsigned long long*>(base + o_bidw);
     A.touched = reinterpret_cast<int32_t*>(base + o_touch);
     A.list = reinterpret_cast<int32_t*>(base + o_list);
+    A.miss = reinterpret_cast<int32_t*>(base + o_miss);
     A.bidj = reinterpret_cast<int32_t*>(base + o_bidj);
     A.bidpk = reinterpret_cast<unsigned long long*>(base + o_bidpk);
-    A.cj = reinterpret_cast<int32_t*>(base + o_cj);
-    A.ca = reinterpret_cast<int64_t*>(base + o_ca);
-    A.cthr = reinterpret_cast<int64_t*>(base + o_cthr);
-    A.cvalid = reinterpret_cast<int32_t*>(base + o_cvalid);
+    A.cache = reinterpret_cast<PCache*>(base + o_cache);
     A.SC = n + 1;
     A.theta = theta < 2 ? 2 : theta;
     A.tail_max = tail_max < 0 ? 0 : (tail_max > kTailMax ? kTailMax : tail_max);
     A.idbits = 1;
     while ((1ll << A.idbits) <= n) ++A.idbits;
+    A.idmask = (1ull << A.idbits) - 1ull;
+    A.koff = 1ll << (62 - A.idbits);
 
     MUX_CUDA_TRY(cudaMemsetAsync(A.cnt, 0, sizeof(AucCounters), st));
     MUX_CUDA_TRY(cudaMemsetAsync(A.price, 0, 8ull * n_pad, st));
-    MUX_CUDA_TRY(cudaMemsetAsync(A.cvalid, 0, 4ull * n_pad, st));
+    MUX_CUDA_TRY(cudaMemsetAsync(A.cache, 0, sizeof(PCache) * (size_t)n_pad, st));
     int64_t launches = 0;
     if (N > 0 && M > 0) {
         dim3 g((unsigned)std::min<int64_t>((M + 255) / 256, 64), (unsigned)std::min<int64_t>(N, 4096));
@@ -601,7 +905,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     if (hc.errors & (1u << 8)) { set_error("mux_match: negative weight"); return MUX_EINVAL; }
     const long long maxq = hc.max_q;
-    // price bound: prices stay below max benefit + n * eps0 <= 2^(63 - idbits)
+    // value/price bound: |v|, p < 2^(62 - idbits) keeps keys and bids in 64 bits
     const double maxa = (double)maxq * (double)A.SC;
     if (maxa * 4.0 + 16.0 >= std::ldexp(1.0, 62 - A.idbits)) {
         set_error("mux_match: weights too large for 64-bit bid packing (reduce qbits)");
@@ -611,20 +915,26 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     if (A.eps0 < 1) A.eps0 = 1;
     A.round_guard = 200000000ll;
 
-    int dev;
-    MUX_CUDA_TRY(cudaGetDevice(&dev));
+    // shared memory: two row buffers + price/owner mirrors when they fit
+    const size_t rows_bytes = 2ull * (size_t)row_bytes;
+    const size_t mirror = (size_t)n_pad * (sizeof(int64_t) + sizeof(int32_t));
+    const char* no_smem = getenv("MUX_NO_SMEM");   // test hook: force the global-memory path
+    const bool smem_mode = rows_bytes + mirror + sizeof(Shared) + 1024 <= kSmemBudget && !(no_smem && *no_smem == '1');
+    const size_t dsmem = smem_mode ? rows_bytes + mirror : 0;
+    void* fn;
+    if (wtype == MUX_W_I32) fn = smem_mode ? (void*)auction_kernel<MUX_W_I32, true> : (void*)auction_kernel<MUX_W_I32, false>;
+    else fn = smem_mode ? (void*)auction_kernel<MUX_W_I64, true> : (void*)auction_kernel<MUX_W_I64, false>;
+    MUX_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     int per_sm = 0;
-    void* fn = wtype == MUX_W_I32 ? (void*)auction_kernel<MUX_W_I32> : (void*)auction_kernel<MUX_W_I64>;
-    MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kAucThreads, 0));
+    MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kAucThreads, dsmem));
     if (per_sm < 1) { set_error("auction kernel cannot be resident"); return MUX_ECUDA; }
-    per_sm = per_sm > 2 ? 2 : per_sm;
-    dim3 grid((unsigned)(ctx->num_sms * per_sm)), block(kAucThreads);
+    dim3 grid((unsigned)ctx->num_sms), block(kAucThreads);
     void* args[] = {&A};
     cudaEvent_t e0, e1;
     MUX_CUDA_TRY(cudaEventCreate(&e0));
     MUX_CUDA_TRY(cudaEventCreate(&e1));
     MUX_CUDA_TRY(cudaEventRecord(e0, st));
-    MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, 0, st));
+    MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, dsmem, st));
     ++launches;
     MUX_CUDA_TRY(cudaEventRecord(e1, st));
     if (N > 0) {
@@ -650,7 +960,14 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         stats->bids = (int64_t)hc.bids; stats->row_scans = (int64_t)hc.scans;
         stats->tail_bids = (int64_t)hc.tail_bids; stats->total_q = hc.total_q;
         stats->ms_match = ms;
+        stats->ms_tail = hc.ns_tail * 1e-6;
+        stats->ms_kernel = hc.ns_total * 1e-6;
+        stats->cache_hits = (int64_t)hc.hits;
         stats->launches += launches;
+        if (getenv("MUX_VERBOSE"))
+            fprintf(stderr, "[mux] tail: scans %llu hit_ms %.2f scan_ms %.2f wait_ms %.2f | rounds: a1 %.2f a2 %.2f b %.2f ms\n",
+                    hc.tail_scans, hc.ns_tail_hit * 1e-6, hc.ns_tail_scan * 1e-6, hc.ns_tail_wait * 1e-6,
+                    hc.ns_a1 * 1e-6, hc.ns_a2 * 1e-6, hc.ns_b * 1e-6);
     }
     return MUX_OK;
 }

@@ -1,0 +1,349 @@
+// MLP speed-predictor plugin: every (online, offline) pair through
+// in(9) -> 64 -> 64 -> 64 -> 1, layers 2 and 3 on the 5th-gen tensor cores.
+//
+// The reference has no MLP (its predictor is the table, predictor.py:85-118);
+// the paper's is "four layers with hidden size 64x64".  The
+// pair-feature build exploits that layer 1 is separable:
+//   W1 [on; off; s] + b1 = P[u] + Q[v],  P = W1_on on_u + W1_s s_u + b1,  Q = W1_off off_v
+// so per pair only relu(P[u] + Q[v]) is formed (CUDA cores, written straight
+// into the UMMA shared-memory layout as bf16).  Per tile of 128 pairs (one
+// online row u x 128 offline columns):
+//   h1 (smem, bf16) --tcgen05.mma x4 (M128 N64 K16, W2 in smem)--> TMEM cols [0,64)
+//   epilogue 1: tcgen05.ld -> +b2, ReLU -> bf16 -> smem (A operand of layer 3)
+//   h2 (smem) --tcgen05.mma x4 (W3)--> TMEM cols [64,128)
+//   epilogue 2: tcgen05.ld -> +b3, ReLU -> dot w4 + b4 -> clamp [0,1] -> store
+// Accumulation is fp32 in TMEM.  One elected thread issues the MMAs and
+// commits them to an mbarrier; four CTAs share an SM (128 TMEM columns each)
+// so one CTA's MMAs overlap the others' CUDA-core stages.
+// Operands use the K-major, no-swizzle canonical layout: 8-row x 16-byte core
+// matrices, LBO = 128 B between K-adjacent cores, SBO = 1024 B between 8-row
+// groups (one 8-row group holds all 64 K values).
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace mux {
+
+constexpr int kH = 64;              // hidden width
+constexpr int kTile = 128;          // pairs per MMA tile (UMMA M)
+constexpr int kMlpThreads = 128;    // 4 warps = the 4 TMEM lane quadrants
+constexpr uint32_t kTmemCols = 128;
+
+struct MlpDev {
+    const float* P;          // [n][64] per-row layer-1 partial (incl. b1)
+    const float* Q;          // [m][64] per-column layer-1 partial
+    const uint16_t* W2c;     // [64*64] bf16 bits, UMMA core layout
+    const uint16_t* W3c;
+    const float* b2;
+    const float* b3;
+    const float* w4;
+    float b4;
+    int32_t n, m;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE (sm_100 version 1).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, K-major A and B.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+        :: "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc) : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(su32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra W_%=;\n}\n" :: "r"(su32(bar)), "r"(parity) : "memory");
+}
+
+// 16 consecutive fp32 columns of this warp's 32 TMEM lanes.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = __uint_as_float(r[t]);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// byte offset of core chunk (row r, k-group kg) in a 128 x 64 K-major tile
+__device__ __forceinline__ uint32_t core_off(int r, int kg) {
+    return (uint32_t)((r >> 3) * 1024 + kg * 128 + (r & 7) * 16);
+}
+
+template <int WT>
+__global__ void __launch_bounds__(kMlpThreads, 4)
+mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
+    __shared__ __align__(1024) unsigned char sA[kTile * kH * 2];      // 16 KB
+    __shared__ __align__(1024) unsigned char sW2[kH * kH * 2];        // 8 KB
+    __shared__ __align__(1024) unsigned char sW3[kH * kH * 2];
+    __shared__ float sP[kH], sb2[kH], sb3[kH], sw4[kH];
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    for (int e = tid; e < kH * kH / 8; e += kMlpThreads) {
+        reinterpret_cast<uint4*>(sW2)[e] = reinterpret_cast<const uint4*>(p.W2c)[e];
+        reinterpret_cast<uint4*>(sW3)[e] = reinterpret_cast<const uint4*>(p.W3c)[e];
+    }
+    if (tid < kH) { sb2[tid] = p.b2[tid]; sb3[tid] = p.b3[tid]; sw4[tid] = p.w4[tid]; }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(su32(&tmem_base)), "r"(kTmemCols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) bar_init(&mbar);
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t idesc = idesc_bf16(kTile, kH);
+    const uint32_t a_addr = su32(sA), w2_addr = su32(sW2), w3_addr = su32(sW3);
+    uint32_t phase = 0;
+
+    const int64_t tpr = (p.m + kTile - 1) / kTile;
+    const int64_t ntiles = (int64_t)p.n * tpr;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int32_t u = (int32_t)(tile / tpr);
+        const int32_t v0 = (int32_t)(tile % tpr) * kTile;
+        if (tid < kH / 4) reinterpret_cast<float4*>(sP)[tid] = __ldg(reinterpret_cast<const float4*>(p.P + (int64_t)u * kH) + tid);
+        __syncthreads();
+        // ---- h1 = relu(P[u] + Q[v]) -> bf16, chunk c = (row r, k-group kg)
+#pragma unroll 2
+        for (int c = tid; c < kTile * 8; c += kMlpThreads) {
+            const int r = (c & 7) | ((c >> 6) << 3);
+            const int kg = (c >> 3) & 7;
+            const int v = v0 + r;
+            uint4 pk = make_uint4(0, 0, 0, 0);
+            if (v < p.m) {
+                const float4* q = reinterpret_cast<const float4*>(p.Q + (int64_t)v * kH + kg * 8);
+                const float4 q0 = __ldg(q), q1 = __ldg(q + 1);
+                const float4 p0 = reinterpret_cast<const float4*>(sP + kg * 8)[0];
+                const float4 p1 = reinterpret_cast<const float4*>(sP + kg * 8)[1];
+                pk.x = pack_bf16(fmaxf(p0.x + q0.x, 0.f), fmaxf(p0.y + q0.y, 0.f));
+                pk.y = pack_bf16(fmaxf(p0.z + q0.z, 0.f), fmaxf(p0.w + q0.w, 0.f));
+                pk.z = pack_bf16(fmaxf(p1.x + q1.x, 0.f), fmaxf(p1.y + q1.y, 0.f));
+                pk.w = pack_bf16(fmaxf(p1.z + q1.z, 0.f), fmaxf(p1.w + q1.w, 0.f));
+            }
+            *reinterpret_cast<uint4*>(sA + core_off(r, kg)) = pk;
+        }
+        fence_async_smem();
+        __syncthreads();
+        // ---- layer 2 on the tensor cores
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < kH / 16; ++ks)
+                mma_bf16(tmem, umma_desc(a_addr + ks * 256, 128, 1024), umma_desc(w2_addr + ks * 256, 128, 1024),
+                         idesc, ks > 0);
+            mma_commit(&mbar);
+        }
+        bar_wait(&mbar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        // ---- epilogue 1: +b2, ReLU -> bf16 -> A operand of layer 3 (own row)
+        const int row = tid;
+#pragma unroll
+        for (int cb = 0; cb < kH / 16; ++cb) {
+            float acc[16];
+            tmem_ld16(tmem + lane_base + cb * 16, acc);
+            tmem_wait_ld();
+            uint4 lo, hi;
+            lo.x = pack_bf16(fmaxf(acc[0] + sb2[cb * 16 + 0], 0.f), fmaxf(acc[1] + sb2[cb * 16 + 1], 0.f));
+            lo.y = pack_bf16(fmaxf(acc[2] + sb2[cb * 16 + 2], 0.f), fmaxf(acc[3] + sb2[cb * 16 + 3], 0.f));
+            lo.z = pack_bf16(fmaxf(acc[4] + sb2[cb * 16 + 4], 0.f), fmaxf(acc[5] + sb2[cb * 16 + 5], 0.f));
+            lo.w = pack_bf16(fmaxf(acc[6] + sb2[cb * 16 + 6], 0.f), fmaxf(acc[7] + sb2[cb * 16 + 7], 0.f));
+            hi.x = pack_bf16(fmaxf(acc[8] + sb2[cb * 16 + 8], 0.f), fmaxf(acc[9] + sb2[cb * 16 + 9], 0.f));
+            hi.y = pack_bf16(fmaxf(acc[10] + sb2[cb * 16 + 10], 0.f), fmaxf(acc[11] + sb2[cb * 16 + 11], 0.f));
+            hi.z = pack_bf16(fmaxf(acc[12] + sb2[cb * 16 + 12], 0.f), fmaxf(acc[13] + sb2[cb * 16 + 13], 0.f));
+            hi.w = pack_bf16(fmaxf(acc[14] + sb2[cb * 16 + 14], 0.f), fmaxf(acc[15] + sb2[cb * 16 + 15], 0.f));
+            *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2)) = lo;
+            *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 1)) = hi;
+        }
+        tc_fence_before();
+        fence_async_smem();
+        __syncthreads();
+        // ---- layer 3 on the tensor cores
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < kH / 16; ++ks)
+                mma_bf16(tmem + kH, umma_desc(a_addr + ks * 256, 128, 1024), umma_desc(w3_addr + ks * 256, 128, 1024),
+                         idesc, ks > 0);
+            mma_commit(&mbar);
+        }
+        bar_wait(&mbar, phase);
+        phase ^= 1;
+        tc_fence_after();
+        // ---- epilogue 2: +b3, ReLU, dot w4 + b4, clamp, store
+        float o = p.b4;
+#pragma unroll
+        for (int cb = 0; cb < kH / 16; ++cb) {
+            float acc[16];
+            tmem_ld16(tmem + lane_base + kH + cb * 16, acc);
+            tmem_wait_ld();
+#pragma unroll
+            for (int t = 0; t < 16; ++t) o = fmaf(fmaxf(acc[t] + sb3[cb * 16 + t], 0.f), sw4[cb * 16 + t], o);
+        }
+        o = fminf(1.f, fmaxf(0.f, o));
+        const int v = v0 + row;
+        if (v < p.m) {
+            if (WT == MUX_W_F32) static_cast<float*>(out)[(int64_t)u * ldo + v] = o;
+            else {
+                const double w = o < 1e-6f ? 0.0 : (double)o;
+                static_cast<int32_t*>(out)[(int64_t)u * ldo + v] = (int32_t)__double2ll_rn(w * qscale);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(kTmemCols) : "memory");
+    }
+}
+
+// layer-1 partials: P[u] = W1_on x_on + W1_s s + b1, Q[v] = W1_off x_off (fp32)
+struct MlpL1 {
+    float W1[kH * 9];
+    float b1[kH];
+    float shift[9];
+    float scale[9];
+};
+
+__global__ void mlp_layer1_kernel(MlpL1 w, const double* __restrict__ on, const double* __restrict__ share,
+                                  int32_t n, const double* __restrict__ off, int32_t m,
+                                  float* __restrict__ P, float* __restrict__ Q) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)(n + m) * kH;
+    if (t >= total) return;
+    const int64_t row = t / kH;
+    const int k = (int)(t % kH);
+    if (row < n) {
+        float acc = w.b1[k];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) acc += w.W1[k * 9 + f] * (float)((on[row * 4 + f] - w.shift[f]) * w.scale[f]);
+        acc += w.W1[k * 9 + 8] * (float)((share[row] - w.shift[8]) * w.scale[8]);
+        P[row * kH + k] = acc;
+    } else {
+        const int64_t v = row - n;
+        float acc = 0.f;
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+            acc += w.W1[k * 9 + 4 + f] * (float)((off[v * 4 + f] - w.shift[4 + f]) * w.scale[4 + f]);
+        Q[v * kH + k] = acc;
+    }
+}
+
+}  // namespace mux
+
+using namespace mux;
+
+// fp32 -> bf16 bits, round to nearest even (host)
+static uint16_t bf16_bits(float f) {
+    uint32_t x;
+    memcpy(&x, &f, 4);
+    const uint32_t lsb = (x >> 16) & 1u;
+    x += 0x7FFFu + lsb;
+    return (uint16_t)(x >> 16);
+}
+
+// W [64 out][64 in] row-major -> UMMA K-major core layout (B operand, N = out)
+static void to_core_layout(const float* W, uint16_t* dst) {
+    for (int nn = 0; nn < kH; ++nn)
+        for (int k = 0; k < kH; ++k) {
+            const size_t off = (size_t)(nn >> 3) * 512 + (size_t)(k >> 3) * 64 + (size_t)(nn & 7) * 8 + (k & 7);
+            dst[off] = bf16_bits(W[nn * kH + k]);
+        }
+}
+
+int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, const double* share, int64_t n,
+                       const double* off, int64_t m, int wtype, int qbits, void* out, int64_t ldo,
+                       cudaStream_t st, int64_t* launches) {
+    if (w->hidden != kH) { set_error("mux_score_mlp: hidden width must be 64"); return MUX_EINVAL; }
+    // parameter block on device: W2c, W3c (bf16 core layout), b2, b3, w4
+    const size_t o_w2 = 0, o_w3 = o_w2 + kH * kH * 2, o_b2 = o_w3 + kH * kH * 2, o_b3 = o_b2 + kH * 4,
+                 o_w4 = o_b3 + kH * 4, o_end = o_w4 + kH * 4;
+    std::string blob(o_end, '\0');
+    to_core_layout(w->W2, reinterpret_cast<uint16_t*>(&blob[o_w2]));
+    to_core_layout(w->W3, reinterpret_cast<uint16_t*>(&blob[o_w3]));
+    memcpy(&blob[o_b2], w->b2, kH * 4);
+    memcpy(&blob[o_b3], w->b3, kH * 4);
+    memcpy(&blob[o_w4], w->w4, kH * 4);
+    const size_t pq_bytes = sizeof(float) * kH * (size_t)(n + m);
+    MUX_TRY(ctx->mlp.ensure(o_end + 256 + pq_bytes));
+    char* base = ctx->mlp.as<char>();
+    MUX_CUDA_TRY(cudaMemcpyAsync(base, blob.data(), o_end, cudaMemcpyHostToDevice, st));
+    float* P = reinterpret_cast<float*>(base + ((o_end + 255) / 256) * 256);
+    float* Q = P + (size_t)kH * n;
+    MlpL1 l1;
+    memcpy(l1.W1, w->W1, sizeof(l1.W1));
+    memcpy(l1.b1, w->b1, sizeof(l1.b1));
+    memcpy(l1.shift, w->shift, sizeof(l1.shift));
+    memcpy(l1.scale, w->scale, sizeof(l1.scale));
+    const int64_t total = (n + m) * kH;
+    if (total > 0) {
+        mlp_layer1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(l1, on, share, (int32_t)n, off, (int32_t)m, P, Q);
+        ++*launches;
+    }
+    MlpDev p;
+    p.P = P; p.Q = Q;
+    p.W2c = reinterpret_cast<const uint16_t*>(base + o_w2);
+    p.W3c = reinterpret_cast<const uint16_t*>(base + o_w3);
+    p.b2 = reinterpret_cast<const float*>(base + o_b2);
+    p.b3 = reinterpret_cast<const float*>(base + o_b3);
+    p.w4 = reinterpret_cast<const float*>(base + o_w4);
+    p.b4 = w->b4;
+    p.n = (int32_t)n; p.m = (int32_t)m;
+    const int64_t tiles = n * ((m + kTile - 1) / kTile);
+    if (tiles > 0) {
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * 4);
+        const double qscale = ldexp(1.0, qbits);
+        if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+        else mlp_pairs_kernel<MUX_W_I32><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+        ++*launches;
+    }
+    MUX_CUDA_TRY(cudaGetLastError());
+    return MUX_OK;
+}

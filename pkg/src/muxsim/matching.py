@@ -1,0 +1,5 @@
+"""muxsim.matching drop-in: re-exports paper_2303_13803_b200.matching (GPU path)."""
+from paper_2303_13803_b200.matching import *  # noqa: F401,F403
+from paper_2303_13803_b200 import matching as _m
+
+globals().update({k: getattr(_m, k) for k in dir(_m) if not k.startswith("__")})

@@ -226,3 +226,39 @@ def test_round_total_matches_oracle(cuda, n, m, seed):
     want, _ = matching_ref.max_weight_total_int(Q)
     assert total == want
     assert matching_ref.assignment_total_int(Q, col) == want
+
+
+def test_global_memory_path(cuda, monkeypatch):
+    """The solver path used when prices/rows do not fit shared memory."""
+    monkeypatch.setenv("MUX_NO_SMEM", "1")
+    for n, m, seed in ((300, 300, 7), (150, 420, 8)):
+        _, Q = _pred_Q(n, m, seed, 20)
+        col, total = _gpu_match(Q)
+        want, _ = matching_ref.max_weight_total_int(Q)
+        assert total == want
+
+
+def test_tail_thresholds(cuda, monkeypatch):
+    """Results stay optimal whatever share of the work the single-CTA tail takes."""
+    _, Q = _pred_Q(400, 400, 9, 20)
+    want, _ = matching_ref.max_weight_total_int(Q)
+    for tail in ("0", "4", "64"):
+        monkeypatch.setenv("MUX_TAIL", tail)
+        _, total = _gpu_match(Q)
+        assert total == want, tail
+
+
+@pytest.mark.parametrize("kind,n", [("uniform", 2500), ("predictor", 2100)])
+def test_large_totals_vs_scipy(cuda, kind, n):
+    """Sizes past the 16 x 128-column threshold exercise the threshold top-K
+    selection; scipy's exact LSA (cross-checked against the reference on
+    dyadic weights) is the oracle here."""
+    from scipy.optimize import linear_sum_assignment
+    if kind == "uniform":
+        Q = np.random.default_rng(1).integers(1, 2 ** 20, size=(n, n), dtype=np.int64)
+    else:
+        _, Q = _pred_Q(n, n, 5, 20)
+    r, c = linear_sum_assignment(Q, maximize=True)
+    col, total = _gpu_match(Q)
+    assert total == int(Q[r, c].sum())
+    assert matching_ref.assignment_total_int(Q, col) == total
