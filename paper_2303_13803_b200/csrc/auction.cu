@@ -65,6 +65,7 @@ struct AucCounters {
     unsigned long long tail_scans;
     long long max_q;
     long long total_q;
+    unsigned long long or_q;
 };
 
 // Per-person candidate cache: one 128-byte record, read by a single lane
@@ -86,6 +87,7 @@ struct AucArgs {
     unsigned long long idmask;
     int64_t koff;        // value offset making keys non-negative
     int64_t SC;          // benefit scale (n + 1)
+    int32_t qshift;      // common power of two divided out of every weight
     int64_t eps0;
     int32_t theta;
     int32_t tail_max;
@@ -164,8 +166,8 @@ __device__ __forceinline__ unsigned long long warp_merge(TopKeys& L, int lane) {
 template <int WT>
 __device__ __forceinline__ int64_t wload1(const AucArgs& A, int32_t i, int32_t j) {
     if (i >= A.N || j >= A.M) return 0;
-    if (WT == MUX_W_I32) return (int64_t)__ldg(static_cast<const int32_t*>(A.W) + (int64_t)i * A.ldw + j);
-    return __ldg(static_cast<const int64_t*>(A.W) + (int64_t)i * A.ldw + j);
+    if (WT == MUX_W_I32) return (int64_t)__ldg(static_cast<const int32_t*>(A.W) + (int64_t)i * A.ldw + j) >> A.qshift;
+    return __ldg(static_cast<const int64_t*>(A.W) + (int64_t)i * A.ldw + j) >> A.qshift;
 }
 
 // 4 consecutive weights of row i starting at column c (c % 4 == 0), read from
@@ -190,10 +192,8 @@ __device__ __forceinline__ void wget4(const AucArgs& A, const void* row, int32_t
         }
         q[0] = a.x; q[1] = a.y; q[2] = b.x; q[3] = b.y;
     }
-    if (c + 4 > A.M) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) if (c + t >= A.M) q[t] = 0;
-    }
+    for (int t = 0; t < 4; ++t) q[t] = (c + t < A.M) ? (q[t] >> A.qshift) : 0;
 }
 
 // ---- prices -------------------------------------------------------------------
@@ -371,14 +371,28 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
     const bool fast = A.n > (kK * 128);   // >= K+1 warps hold columns
     bool done = false;
     if (fast) {
-        unsigned long long mx = kNoKey;
-        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4) {
-            unsigned long long k[4];
-            keys4<WT, SP>(A, P, row, i, c, k);
+        // pass 1: per-thread best (value, lowest index) and per-group maxima
+        constexpr int kGroups = 8;           // 4-column groups cached per thread (n <= 16384)
+        int64_t gmax[kGroups];
+        int64_t bv = kNegInf;
+        int32_t bj = INT32_MAX;
+        int g = 0;
+        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4, ++g) {
+            int64_t q[4], pr[4];
+            wget4<WT>(A, row, i, c, q);
+            pget4<SP>(P, c, pr);
+            int64_t gm = kNegInf;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) mx = k[t] > mx ? k[t] : mx;
+            for (int t = 0; t < 4; ++t) {
+                if (c + t >= A.n) continue;
+                const int64_t v = q[t] * A.SC - pr[t];
+                gm = v > gm ? v : gm;
+                if (v > bv) { bv = v; bj = c + t; }   // columns ascend: strict > keeps the lowest index
+            }
+#pragma unroll
+            for (int k = 0; k < kGroups; ++k) if (k == g) gmax[k] = gm;
         }
-        mx = warp_max_u64(mx);
+        const unsigned long long mx = warp_max_u64(bj == INT32_MAX ? kNoKey : mkkey(A, bv, bj));
         if (lane == 0) S.wmax[warp] = mx;
         if (threadIdx.x == 0) S.ncand = 0;
         __syncthreads();
@@ -393,8 +407,18 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
             if (rank == kK) S.tau = v;
         }
         __syncthreads();
+        // pass 2: collect keys >= tau, revisiting only groups that can reach it
         const unsigned long long tau = S.tau;
-        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4) {
+        const int64_t tau_v = key_v(A, tau);
+        const bool cached = g <= kGroups;
+        g = 0;
+        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4, ++g) {
+            if (cached) {
+                int64_t gm = kNegInf;
+#pragma unroll
+                for (int k = 0; k < kGroups; ++k) if (k == g) gm = gmax[k];
+                if (gm < tau_v) continue;
+            }
             unsigned long long k[4];
             keys4<WT, SP>(A, P, row, i, c, k);
 #pragma unroll
@@ -446,7 +470,13 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
             const bool ok = mk != kNoKey;
             const int32_t j = ok ? key_j(A, mk) : -1;
             rec->j[lane] = j;
-            rec->q[lane] = ok ? (key_v(A, mk) + pget<SP>(P, j)) / A.SC : 0;
+            int64_t q = 0;
+            if (ok && i < A.N && j < A.M) {
+                if (row) q = (WT == MUX_W_I32 ? (int64_t)static_cast<const int32_t*>(row)[j]
+                                              : static_cast<const int64_t*>(row)[j]) >> A.qshift;
+                else q = wload1<WT>(A, i, j);
+            }
+            rec->q[lane] = q;
         }
         if (lane == 0) {
             const unsigned long long k0 = S.sel[0], k1 = S.sel[1], kt = S.sel[kK];
@@ -788,13 +818,18 @@ auction_kernel(AucArgs A) {
 template <int WT>
 __global__ void max_q_kernel(const void* W, int64_t ldw, int32_t N, int32_t M, AucCounters* cnt) {
     long long mx = 0;
+    unsigned long long orv = 0;
     for (int64_t r = blockIdx.y; r < N; r += gridDim.y)
         for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < M; c += (int64_t)gridDim.x * blockDim.x) {
             long long q = (WT == MUX_W_I32) ? (long long)static_cast<const int32_t*>(W)[r * ldw + c]
                                             : static_cast<const int64_t*>(W)[r * ldw + c];
             mx = q > mx ? q : mx;
+            orv |= (unsigned long long)q;
             if (q < 0) atomicOr(&cnt->errors, 1u << 8);
         }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) orv |= __shfl_xor_sync(0xffffffffu, orv, o);
+    if ((threadIdx.x & 31) == 0 && orv) atomicOr(&cnt->or_q, orv);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         long long o2 = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -904,7 +939,11 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     MUX_CUDA_TRY(cudaMemcpyAsync(&hc, A.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     if (hc.errors & (1u << 8)) { set_error("mux_match: negative weight"); return MUX_EINVAL; }
-    const long long maxq = hc.max_q;
+    // divide out the common power of two: the solve is then exactly invariant
+    // to power-of-two weight scaling (the reference's scale-invariance test)
+    A.qshift = 0;
+    if (hc.or_q) while (((hc.or_q >> A.qshift) & 1ull) == 0) ++A.qshift;
+    const long long maxq = hc.max_q >> A.qshift;
     // value/price bound: |v|, p < 2^(62 - idbits) keeps keys and bids in 64 bits
     const double maxa = (double)maxq * (double)A.SC;
     if (maxa * 4.0 + 16.0 >= std::ldexp(1.0, 62 - A.idbits)) {

@@ -262,3 +262,62 @@ def test_large_totals_vs_scipy(cuda, kind, n):
     col, total = _gpu_match(Q)
     assert total == int(Q[r, c].sum())
     assert matching_ref.assignment_total_int(Q, col) == total
+
+
+def test_scale_invariance_of_pair_choice(cuda):
+    """pkg/tests/test_matching.py:116-125: x4 weights -> same pairs, total x4."""
+    from paper_2303_13803_b200 import BipartiteGraph, max_weight_matching
+    rng = random.Random(5)
+    for _ in range(100):
+        nl, nr = rng.randint(0, 5), rng.randint(0, 5)
+        L = tuple(f"l{i}" for i in range(nl))
+        R = tuple(f"r{j}" for j in range(nr))
+        w = {(l, r): rng.randrange(65) / 64 for l in L for r in R if rng.random() < 0.7}
+        g = BipartiteGraph(L, R, w)
+        m1 = max_weight_matching(g)
+        m2 = max_weight_matching(BipartiteGraph(L, R, {e: 4.0 * x for e, x in w.items()}))
+        assert m1.pairs == m2.pairs
+        assert m2.total_weight == 4.0 * m1.total_weight
+
+
+def test_deterministic_across_input_orderings(cuda):
+    """pkg/tests/test_matching.py:89-103."""
+    from paper_2303_13803_b200 import BipartiteGraph, max_weight_matching
+    rng = random.Random(99)
+    for _ in range(200):
+        nl, nr = rng.randint(0, 5), rng.randint(0, 5)
+        L = [f"l{i}" for i in range(nl)]
+        R = [f"r{j}" for j in range(nr)]
+        w = {(l, r): rng.randrange(65) / 64 for l in L for r in R if rng.random() < 0.7}
+        m1 = max_weight_matching(BipartiteGraph(tuple(L), tuple(R), w))
+        rng.shuffle(L)
+        rng.shuffle(R)
+        items = list(w.items())
+        rng.shuffle(items)
+        m2 = max_weight_matching(BipartiteGraph(tuple(L), tuple(R), dict(items)))
+        assert m1 == m2
+
+
+def test_golden_pairs_where_optimum_unique(cuda, golden):
+    """Identical pair lists wherever the reference's optimum is unique."""
+    from paper_2303_13803_b200 import max_weight_matching
+    checked = 0
+    for case in golden["matching"]["cases"]:
+        L, R = sorted(case["left"]), sorted(case["right"])
+        if not L or not R:
+            continue
+        li = {l: i for i, l in enumerate(L)}
+        ri = {r: j for j, r in enumerate(R)}
+        n = max(len(L), len(R))
+        Q = np.zeros((n, n), dtype=np.int64)
+        for a, b, x in case["edges"]:
+            if x >= 1e-6:
+                Q[li[a], ri[b]] = round(x * 64)
+        cost = Q.max() - Q
+        col, u, v = matching_ref.solve_min_assignment(cost)
+        if not matching_ref.is_unique_optimum(cost, col, u, v):
+            continue
+        m = max_weight_matching(_graph_from_case(case))
+        assert [list(p) for p in m.pairs] == case["pairs"]
+        checked += 1
+    assert checked >= 20
