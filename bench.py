@@ -48,7 +48,16 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-mlp", action="store_true")
     return p.parse_args()
+
+
+def bf16_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["bf16_tflops"]
+    except Exception:
+        return 1590.0
 
 
 def peaks():
@@ -269,6 +278,39 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": e2e_ms / world, "unit": "ms", "h2d_bytes_per_step": (2 * n + m) * 8 * world,
                "d2h_bytes_per_step": n * 4 * world, "per_round_ms": e2e_ms}
 
+    # MLP plugin (tcgen05) scoring of the same N x M pairs: tensor-core roofline
+    mlp_line = None
+    if not args.no_mlp:
+        from paper_2303_13803_b200.mlp import MlpPredictor
+        mlp = MlpPredictor.random(args.seed)
+        rng = np.random.default_rng(args.seed)
+        on = torch.as_tensor(np.stack([np.minimum(1.0, 1.8 * cl.x), cl.x, np.full(n, 0.5),
+                                       rng.uniform(0.01, 0.04, n)], axis=1), device=dev)
+        off = torch.as_tensor(np.stack([np.minimum(1.0, 1.8 * cl.y), cl.y, np.full(m, 0.5),
+                                        np.full(m, 0.1)], axis=1), device=dev)
+        Wm = torch.empty((n, ldw), dtype=torch.float32, device=dev)
+        st_m, keep_m = mlp.struct()
+
+        def mlp_step():
+            nat.check(lib.mux_score_mlp(ctx, nat.ctypes.byref(st_m), on.data_ptr(), sd.data_ptr(), n,
+                                        off.data_ptr(), m, nat.MUX_W_F32, 0, Wm.data_ptr(), ldw, sptr))
+        for _ in range(2):
+            mlp_step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mlp_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        mlp_ms = sorted(ts)[len(ts) // 2]
+        flops = 2.0 * 64 * 64 * 2 * n * m + 4.0 * 64 * n * m
+        mlp_line = {"ms": mlp_ms, "tflops": flops / (mlp_ms / 1e3) / 1e12, "flops": flops,
+                    "note": "layers 2-3 as tcgen05 kind::f16 M128xN64xK16, fp32 TMEM accumulate"}
+
     if rank != 0:
         return
     hbm, peak_kind = peaks()
@@ -298,6 +340,10 @@ def run_ours(args, rank, world, local_rank):
         "solver": {k: s[k] for k in ("phases", "rounds", "bids", "row_scans", "tail_bids", "cache_hits", "total_q", "ms_tail", "ms_kernel")},
         "ms_match": auc_ms, "ms_per_step_all": times,
     }
+    if mlp_line is not None:
+        bf16 = bf16_peak()
+        mlp_line.update({"peak_tflops": bf16, "frac": mlp_line["tflops"] / bf16, "bound": "tensor"})
+        line["mlp_plugin"] = mlp_line
     print(json.dumps(line), flush=True)
 
 
@@ -306,18 +352,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        # CPU oracle port: rank 0 alone runs and prints; other ranks exit at once
+        run_reference(args, rank, world)
+        return
     if world > 1:
         import torch
         import torch.distributed as dist
-        if args.impl == "ours":
-            torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl")
-        else:
-            dist.init_process_group("gloo")
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-    else:
-        run_ours(args, rank, world, local_rank)
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

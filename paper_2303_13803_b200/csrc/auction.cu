@@ -60,9 +60,12 @@ struct AucCounters {
     int32_t miss_count;
     uint32_t errors;
     uint32_t tail_epoch;
+    uint32_t bar_count;                 // custom grid barrier
+    uint32_t bar_gen;
     unsigned long long rounds, bids, scans, tail_bids, phases, hits;
     long long ns_total, ns_tail, ns_tail_hit, ns_tail_scan, ns_tail_wait, ns_a1, ns_a2, ns_b;
     unsigned long long tail_scans;
+    long long ns_stage[5];
     long long max_q;
     long long total_q;
     unsigned long long or_q;
@@ -88,6 +91,7 @@ struct AucArgs {
     int64_t koff;        // value offset making keys non-negative
     int64_t SC;          // benefit scale (n + 1)
     int32_t qshift;      // common power of two divided out of every weight
+    int32_t cg_sync;     // 1: cooperative-groups grid.sync, 0: custom barrier
     int64_t eps0;
     int32_t theta;
     int32_t tail_max;
@@ -196,10 +200,31 @@ __device__ __forceinline__ void wget4(const AucArgs& A, const void* row, int32_t
     for (int t = 0; t < 4; ++t) q[t] = (c + t < A.M) ? (q[t] >> A.qshift) : 0;
 }
 
+// ---- explicit shared-memory loads (keep the scan off the generic path) ---------
+
+__device__ __forceinline__ int4 lds_v4(uint32_t a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ longlong2 lds_v2ll(uint32_t a) {
+    longlong2 v;
+    asm volatile("ld.shared.v2.s64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ int64_t lds_ll(uint32_t a) {
+    long long v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+
 // ---- prices -------------------------------------------------------------------
 
 template <bool SP>
-__device__ __forceinline__ int64_t pget(const int64_t* P, int32_t j) { return SP ? P[j] : __ldcg(P + j); }
+__device__ __forceinline__ int64_t pget(const int64_t* P, int32_t j) {
+    return SP ? lds_ll((uint32_t)__cvta_generic_to_shared(P + j)) : __ldcg(P + j);
+}
 
 template <bool SP>
 __device__ __forceinline__ void pget4(const int64_t* P, int32_t c, int64_t (&p)[4]) {
@@ -247,6 +272,28 @@ __device__ __forceinline__ uint64_t gtimer() {
     return t;
 }
 
+// Grid-wide barrier for the persistent kernel: one arrival atomic per CTA, the
+// last arriver bumps a generation word; waiters poll it with relaxed loads
+// (no L1 invalidation per poll) and fence once on exit.
+__device__ __forceinline__ void grid_barrier(const AucArgs& A, cg::grid_group& grid) {
+    if (A.cg_sync) { grid.sync(); return; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile uint32_t* gen = &A.cnt->bar_gen;
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(&A.cnt->bar_count, 1u) == gridDim.x - 1) {
+            A.cnt->bar_count = 0;
+            __threadfence();
+            atomicAdd(&A.cnt->bar_gen, 1u);
+        } else {
+            while (*gen == g) { }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // ---- per-CTA shared state ------------------------------------------------------
 
 struct Shared {
@@ -264,12 +311,15 @@ struct Shared {
     unsigned long long sel[kK + 1];            // selected top-(K+1) keys
     int32_t ncand;
     unsigned long long cand[kCandMax];          // keys >= tau
+    unsigned long long tprof[8];                 // tail stage timers (ns)
 };
 
 struct Dyn {             // carve-up of dynamic shared memory
     int64_t* price;      // [n_pad] price mirror (SP mode)
     int32_t* owner;      // [n_pad] owner mirror (SP mode, tail only)
-    unsigned char* row[2];
+    unsigned char* row0;  // two staged weight rows (double buffer)
+    unsigned char* row1;
+    __device__ __forceinline__ unsigned char* row(int b) const { return b ? row1 : row0; }  // no local array
 };
 
 // Stage the price array (and owners) from global into the CTA's mirror.
@@ -295,14 +345,14 @@ __device__ __forceinline__ void fetch_row(const AucArgs& A, Shared& S, Dyn& D, i
     if (i >= A.N || A.M == 0) return;            // dummy person: no weights to load
     const size_t esz = WT == MUX_W_I32 ? 4 : 8;
     const char* src = static_cast<const char*>(A.W) + (size_t)i * A.ldw * esz;
-    tma_row(&S.bar[b], D.row[b], src, (uint32_t)A.row_bytes);
+    tma_row(&S.bar[b], D.row(b), src, (uint32_t)A.row_bytes);
 }
 // Wait for buffer b (all threads); returns the row pointer.
 template <int WT>
 __device__ __forceinline__ const void* wait_row(const AucArgs& A, Shared& S, Dyn& D, int b, int32_t i) {
-    if (i >= A.N || A.M == 0) return D.row[b];
+    if (i >= A.N || A.M == 0) return D.row(b);
     mbar_wait(&S.bar[b], S.bar_phase[b]);
-    return D.row[b];
+    return D.row(b);
 }
 
 // ---- bids ----------------------------------------------------------------------
@@ -323,15 +373,16 @@ __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, in
     const int32_t valid = (int32_t)(w[6].y & 0xffffffffll);
     if (!valid) return false;
     const int64_t thr = w[6].x;
-    const int32_t* jj = reinterpret_cast<const int32_t*>(&w[0]);
-    const int64_t* qq = reinterpret_cast<const int64_t*>(&w[2]);
     int64_t v1 = kNegInf, v2 = kNegInf, a1 = 0;
     int32_t b = INT32_MAX;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
-        const int32_t j = jj[k];
+        // fields by value (no address-taking, so w[] stays in registers)
+        const long long jw = (k & 2) ? w[k >> 2].y : w[k >> 2].x;
+        const int32_t j = (k & 1) ? (int32_t)(jw >> 32) : (int32_t)(jw & 0xffffffffll);
+        const int64_t qk = (k & 1) ? w[2 + (k >> 1)].y : w[2 + (k >> 1)].x;
         if (j < 0) continue;
-        const int64_t a = qq[k] * A.SC;
+        const int64_t a = qk * A.SC;
         const int64_t v = a - pget<SP>(P, j);
         if (v > v1 || (v == v1 && j < b)) { v2 = v1; v1 = v; b = j; a1 = a; }
         else if (v > v2) v2 = v;
@@ -341,6 +392,32 @@ __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, in
     j1 = b;
     bid = bid_from(a1, v1, s2, eps);
     return true;
+}
+
+// Weights and prices of 4 consecutive columns for the CTA scan.  In
+// shared-memory mode (SP) both come from the CTA's staged row / price mirror
+// through explicit ld.shared; otherwise from global memory.
+template <int WT, bool SP>
+__device__ __forceinline__ void scan_load4(const AucArgs& A, uint32_t row_s, uint32_t price_s, const int64_t* P,
+                                           int32_t i, int32_t c, int64_t (&q)[4], int64_t (&p)[4]) {
+    if (SP) {
+        const longlong2 a = lds_v2ll(price_s + (uint32_t)c * 8u);
+        const longlong2 b = lds_v2ll(price_s + (uint32_t)c * 8u + 16u);
+        p[0] = a.x; p[1] = a.y; p[2] = b.x; p[3] = b.y;
+        if (i >= A.N || c >= A.M) { q[0] = q[1] = q[2] = q[3] = 0; return; }
+        if (WT == MUX_W_I32) {
+            const int4 v = lds_v4(row_s + (uint32_t)c * 4u);
+            q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+        } else {
+            const longlong2 x = lds_v2ll(row_s + (uint32_t)c * 8u), y = lds_v2ll(row_s + (uint32_t)c * 8u + 16u);
+            q[0] = x.x; q[1] = x.y; q[2] = y.x; q[3] = y.y;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) q[t] = (c + t < A.M) ? (q[t] >> A.qshift) : 0;
+    } else {
+        wget4<WT>(A, nullptr, i, c, q);
+        pget4<false>(P, c, p);
+    }
 }
 
 // Key of row i at column c (4 consecutive), zero key for padding columns.
@@ -370,32 +447,51 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool fast = A.n > (kK * 128);   // >= K+1 warps hold columns
     bool done = false;
+    uint64_t tp0 = gtimer();
+#define MUX_STAGE(k) do { if (threadIdx.x == 0) { const uint64_t _t = gtimer(); S.tprof[k] += _t - tp0; tp0 = _t; } } while (0)
     if (fast) {
-        // pass 1: per-thread best (value, lowest index) and per-group maxima
-        constexpr int kGroups = 8;           // 4-column groups cached per thread (n <= 16384)
-        int64_t gmax[kGroups];
+        // pass 1: per-thread best (value, lowest index) and per-group maxima.
+        // kIters fixed-trip steps keep the group maxima in registers; rows
+        // longer than kIters * 2048 columns fall back to a full pass 2.
+        constexpr int kIters = 8;
+        const uint32_t row_s = SP ? smem_u32(row) : 0u;
+        const uint32_t price_s = SP ? smem_u32(P) : 0u;
+        const int32_t stride = kAucThreads * 4;
+        const bool cached = A.n <= kIters * stride;
+        int64_t gmax[kIters];
         int64_t bv = kNegInf;
         int32_t bj = INT32_MAX;
-        int g = 0;
-        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4, ++g) {
+#pragma unroll
+        for (int it = 0; it < kIters; ++it) {
+            const int32_t c = threadIdx.x * 4 + it * stride;
+            gmax[it] = kNegInf;
+            if (c < A.n) {
+                int64_t q[4], pr[4];
+                scan_load4<WT, SP>(A, row_s, price_s, P, i, c, q, pr);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (c + t >= A.n) continue;
+                    const int64_t v = q[t] * A.SC - pr[t];
+                    gmax[it] = v > gmax[it] ? v : gmax[it];
+                    if (v > bv) { bv = v; bj = c + t; }   // columns ascend: strict > keeps the lowest index
+                }
+            }
+        }
+        for (int32_t c = threadIdx.x * 4 + kIters * stride; c < A.n; c += stride) {
             int64_t q[4], pr[4];
-            wget4<WT>(A, row, i, c, q);
-            pget4<SP>(P, c, pr);
-            int64_t gm = kNegInf;
+            scan_load4<WT, SP>(A, row_s, price_s, P, i, c, q, pr);
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 if (c + t >= A.n) continue;
                 const int64_t v = q[t] * A.SC - pr[t];
-                gm = v > gm ? v : gm;
-                if (v > bv) { bv = v; bj = c + t; }   // columns ascend: strict > keeps the lowest index
+                if (v > bv) { bv = v; bj = c + t; }
             }
-#pragma unroll
-            for (int k = 0; k < kGroups; ++k) if (k == g) gmax[k] = gm;
         }
         const unsigned long long mx = warp_max_u64(bj == INT32_MAX ? kNoKey : mkkey(A, bv, bj));
         if (lane == 0) S.wmax[warp] = mx;
         if (threadIdx.x == 0) S.ncand = 0;
         __syncthreads();
+        MUX_STAGE(0);
         if (warp == 0 && lane < kAucWarps) {
             const unsigned long long v = S.wmax[lane];
             int rank = 0;
@@ -407,28 +503,45 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
             if (rank == kK) S.tau = v;
         }
         __syncthreads();
+        MUX_STAGE(1);
         // pass 2: collect keys >= tau, revisiting only groups that can reach it
         const unsigned long long tau = S.tau;
         const int64_t tau_v = key_v(A, tau);
-        const bool cached = g <= kGroups;
-        g = 0;
-        for (int32_t c = threadIdx.x * 4; c < A.n; c += kAucThreads * 4, ++g) {
-            if (cached) {
-                int64_t gm = kNegInf;
 #pragma unroll
-                for (int k = 0; k < kGroups; ++k) if (k == g) gm = gmax[k];
-                if (gm < tau_v) continue;
-            }
-            unsigned long long k[4];
-            keys4<WT, SP>(A, P, row, i, c, k);
+        for (int it = 0; it < kIters; ++it) {
+            const int32_t c = threadIdx.x * 4 + it * stride;
+            if (c >= A.n || (cached && gmax[it] < tau_v)) continue;
+            int64_t q[4], pr[4];
+            scan_load4<WT, SP>(A, row_s, price_s, P, i, c, q, pr);
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (k[t] >= tau && k[t] != kNoKey) {
+            for (int t = 0; t < 4; ++t) {
+                if (c + t >= A.n) continue;
+                const int64_t v = q[t] * A.SC - pr[t];
+                if (v < tau_v) continue;
+                const unsigned long long k = mkkey(A, v, c + t);
+                if (k >= tau) {
                     const int slot = atomicAdd(&S.ncand, 1);
-                    if (slot < kCandMax) S.cand[slot] = k[t];
+                    if (slot < kCandMax) S.cand[slot] = k;
                 }
+            }
+        }
+        for (int32_t c = threadIdx.x * 4 + kIters * stride; c < A.n; c += stride) {
+            int64_t q[4], pr[4];
+            scan_load4<WT, SP>(A, row_s, price_s, P, i, c, q, pr);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (c + t >= A.n) continue;
+                const int64_t v = q[t] * A.SC - pr[t];
+                if (v < tau_v) continue;
+                const unsigned long long k = mkkey(A, v, c + t);
+                if (k >= tau) {
+                    const int slot = atomicAdd(&S.ncand, 1);
+                    if (slot < kCandMax) S.cand[slot] = k;
+                }
+            }
         }
         __syncthreads();
+        MUX_STAGE(2);
         const int nc = S.ncand;
         if (nc <= kCandMax) {
             for (int t = threadIdx.x; t < nc; t += kAucThreads) {
@@ -462,6 +575,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
         }
     }
     __syncthreads();
+    MUX_STAGE(3);
     if (warp == 0) {
         // cache: lanes 0..K-1 hold ranks 0..K-1, rank K is the threshold
         const unsigned long long mk = lane <= kK ? S.sel[lane] : kNoKey;
@@ -490,6 +604,8 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
         }
     }
     __syncthreads();
+    MUX_STAGE(4);
+#undef MUX_STAGE
 }
 
 __device__ __forceinline__ unsigned long long pack_bid(const AucArgs& A, int64_t bid, int32_t i) {
@@ -624,8 +740,8 @@ auction_kernel(AucArgs A) {
     Dyn D;
     {
         unsigned char* p = dsm;
-        D.row[0] = p; p += A.row_bytes;
-        D.row[1] = p; p += A.row_bytes;
+        D.row0 = p; p += A.row_bytes;
+        D.row1 = p; p += A.row_bytes;
         D.price = reinterpret_cast<int64_t*>(p); p += sizeof(int64_t) * A.n_pad;
         D.owner = reinterpret_cast<int32_t*>(p);
     }
@@ -639,6 +755,7 @@ auction_kernel(AucArgs A) {
         fence_mbar_init();
         S.bar_phase[0] = S.bar_phase[1] = 0;
         S.row_person[0] = S.row_person[1] = -1;
+        for (int k = 0; k < 8; ++k) S.tprof[k] = 0;
     }
     __syncthreads();
     int64_t eps = A.eps0;
@@ -665,7 +782,7 @@ auction_kernel(AucArgs A) {
             A.cnt->miss_count = 0;
             atomicAdd(&A.cnt->phases, 1ull);
         }
-        grid.sync();
+        grid_barrier(A, grid);
         int r = 0;
         for (;;) {
             const int cur = r & 1, nxt = cur ^ 1;
@@ -691,7 +808,7 @@ auction_kernel(AucArgs A) {
                     }
                     __threadfence();
                 }
-                grid.sync();
+                grid_barrier(A, grid);
                 break;
             }
             const int32_t* L = A.list + (int64_t)cur * A.n_pad;
@@ -723,7 +840,7 @@ auction_kernel(AucArgs A) {
                 my_hits += __shfl_xor_sync(0xffffffffu, my_hits, 1);
                 if (lane == 0 && my_hits) atomicAdd(&A.cnt->hits, my_hits);
             }
-            grid.sync();
+            grid_barrier(A, grid);
             const uint64_t tr1 = gtimer();
             // ---- [A2] cooperative row scans for the misses, spread over CTAs
             {
@@ -756,7 +873,7 @@ auction_kernel(AucArgs A) {
                     }
                 }
             }
-            grid.sync();
+            grid_barrier(A, grid);
             const uint64_t tr2 = gtimer();
             // ---- [B] resolve
             {
@@ -787,7 +904,7 @@ auction_kernel(AucArgs A) {
                     }
                 }
             }
-            grid.sync();
+            grid_barrier(A, grid);
             if (gtid == 0) {
                 const uint64_t tr3 = gtimer();
                 t_a1 += tr1 - tr0;
@@ -808,6 +925,7 @@ auction_kernel(AucArgs A) {
     if (gtid == 0) {
         A.cnt->ns_total = (long long)(gtimer() - t_start);
         A.cnt->ns_tail = (long long)t_tail;
+        for (int k = 0; k < 5; ++k) A.cnt->ns_stage[k] = (long long)S.tprof[k];
         A.cnt->ns_a1 = (long long)t_a1;
         A.cnt->ns_a2 = (long long)t_a2;
         A.cnt->ns_b = (long long)t_b;
@@ -953,6 +1071,8 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.eps0 = (int64_t)(maxa / 4.0);
     if (A.eps0 < 1) A.eps0 = 1;
     A.round_guard = 200000000ll;
+    const char* cgs = getenv("MUX_CG_SYNC");
+    A.cg_sync = (cgs && *cgs == '1') ? 1 : 0;
 
     // shared memory: two row buffers + price/owner mirrors when they fit
     const size_t rows_bytes = 2ull * (size_t)row_bytes;
@@ -1007,6 +1127,10 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             fprintf(stderr, "[mux] tail: scans %llu hit_ms %.2f scan_ms %.2f wait_ms %.2f | rounds: a1 %.2f a2 %.2f b %.2f ms\n",
                     hc.tail_scans, hc.ns_tail_hit * 1e-6, hc.ns_tail_scan * 1e-6, hc.ns_tail_wait * 1e-6,
                     hc.ns_a1 * 1e-6, hc.ns_a2 * 1e-6, hc.ns_b * 1e-6);
+        if (getenv("MUX_VERBOSE"))
+            fprintf(stderr, "[mux] CTA0 scan stages ms: pass1 %.2f tau %.2f pass2 %.2f rank %.2f store %.2f\n",
+                    hc.ns_stage[0] * 1e-6, hc.ns_stage[1] * 1e-6, hc.ns_stage[2] * 1e-6, hc.ns_stage[3] * 1e-6,
+                    hc.ns_stage[4] * 1e-6);
     }
     return MUX_OK;
 }

@@ -104,7 +104,16 @@ def max_weight_matching(g: BipartiteGraph, qbits: int = None) -> Matching:
             W[li[l], ri[r]] = w
     if nl == 0 or nr == 0:
         return Matching(pairs=(), total_weight=0.0)
-    q = max_qbits(max(nl, nr)) if qbits is None else int(qbits)
+    if qbits is None:
+        # resolution 2^-q with every rint(w * 2^q) inside int32 and the bid packing
+        wmax = float(W.max())
+        q = max_qbits(max(nl, nr))
+        if wmax > 0:
+            q_int = int(math.floor(math.log2((2 ** 31 - 1) / wmax)))
+            q_pack = q - max(0, int(math.ceil(math.log2(wmax))))
+            q = max(1, min(q_int, q_pack))
+    else:
+        q = int(qbits)
     Q = quantise(W, q)
     ldw = ((nr + 3) // 4) * 4
     Qp = np.zeros((nl, ldw), dtype=np.int32)
