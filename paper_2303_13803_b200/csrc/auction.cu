@@ -45,7 +45,7 @@ namespace cg = cooperative_groups;
 
 namespace mux {
 
-constexpr int kK = 8;                 // cached candidates per person
+constexpr int kK = 15;                // cached candidates per person (K + 1 = 16)
 constexpr int kAucThreads = 512;      // 16 warps per CTA
 constexpr int kAucWarps = kAucThreads / kWarp;
 constexpr int kTailMax = 64;          // largest tail handled by the single CTA
@@ -71,16 +71,17 @@ struct AucCounters {
     unsigned long long or_q;
 };
 
-// Per-person candidate cache: one 128-byte record, read by a single lane
-// with seven 16-byte loads.
-struct __align__(128) PCache {
-    int32_t j[kK];       // cached objects, best first (-1 = empty)
-    int64_t q[kK];       // their weights (benefit = q * SC)
+// Per-person candidate cache: one 256-byte record, read by a single lane
+// with thirteen 16-byte loads.
+struct __align__(256) PCache {
+    int32_t j[16];       // cached objects, best first (-1 = empty; slot 15 unused)
+    int64_t q[16];       // their weights (benefit = q * SC)
     int64_t thr;         // (K+1)-th best value at scan time
     int32_t valid;
-    int32_t pad[3];
+    int32_t pad[11];
 };
-static_assert(sizeof(PCache) == 128, "PCache must be one 128-byte line");
+static_assert(sizeof(PCache) == 256, "PCache must be 256 bytes");
+static_assert(kK <= 15, "PCache holds at most 15 candidates");
 
 struct AucArgs {
     const void* W;       // [N][ldw] int32 or int64
@@ -306,7 +307,7 @@ struct Shared {
     int32_t j1;
     int64_t bid;
     unsigned long long wk[kAucWarps][kK + 1];  // per-warp merged keys (slow path)
-    unsigned long long wmax[kAucWarps];        // per-warp maximum key
+    unsigned long long wmax[2 * kAucWarps];    // per-half-warp maximum key
     unsigned long long tau;                    // selection threshold
     unsigned long long sel[kK + 1];            // selected top-(K+1) keys
     int32_t ncand;
@@ -367,12 +368,12 @@ template <bool SP>
 __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, int32_t i, int64_t eps,
                                           int32_t& j1, int64_t& bid) {
     const longlong2* rec = reinterpret_cast<const longlong2*>(A.cache + i);
-    longlong2 w[7];      // j[0..8) | q[0..8) | thr, valid
+    longlong2 w[13];     // j[0..16) | q[0..16) | thr, valid
 #pragma unroll
-    for (int t = 0; t < 7; ++t) w[t] = __ldcg(rec + t);
-    const int32_t valid = (int32_t)(w[6].y & 0xffffffffll);
+    for (int t = 0; t < 13; ++t) w[t] = __ldcg(rec + t);
+    const int32_t valid = (int32_t)(w[12].y & 0xffffffffll);
     if (!valid) return false;
-    const int64_t thr = w[6].x;
+    const int64_t thr = w[12].x;
     int64_t v1 = kNegInf, v2 = kNegInf, a1 = 0;
     int32_t b = INT32_MAX;
 #pragma unroll
@@ -380,7 +381,7 @@ __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, in
         // fields by value (no address-taking, so w[] stays in registers)
         const long long jw = (k & 2) ? w[k >> 2].y : w[k >> 2].x;
         const int32_t j = (k & 1) ? (int32_t)(jw >> 32) : (int32_t)(jw & 0xffffffffll);
-        const int64_t qk = (k & 1) ? w[2 + (k >> 1)].y : w[2 + (k >> 1)].x;
+        const int64_t qk = (k & 1) ? w[4 + (k >> 1)].y : w[4 + (k >> 1)].x;
         if (j < 0) continue;
         const int64_t a = qk * A.SC;
         const int64_t v = a - pget<SP>(P, j);
@@ -445,7 +446,7 @@ template <int WT, bool SP>
 __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, const void* row, int32_t i,
                              int64_t eps) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool fast = A.n > (kK * 128);   // >= K+1 warps hold columns
+    const bool fast = A.n > (kK * 64);    // >= K+1 half-warps hold columns
     bool done = false;
     uint64_t tp0 = gtimer();
 #define MUX_STAGE(k) do { if (threadIdx.x == 0) { const uint64_t _t = gtimer(); S.tprof[k] += _t - tp0; tp0 = _t; } } while (0)
@@ -487,16 +488,23 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
                 if (v > bv) { bv = v; bj = c + t; }
             }
         }
-        const unsigned long long mx = warp_max_u64(bj == INT32_MAX ? kNoKey : mkkey(A, bv, bj));
-        if (lane == 0) S.wmax[warp] = mx;
+        unsigned long long mx = bj == INT32_MAX ? kNoKey : mkkey(A, bv, bj);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {      // half-warp maximum
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = x > mx ? x : mx;
+        }
+        if ((lane & 15) == 0) S.wmax[warp * 2 + (lane >> 4)] = mx;
         if (threadIdx.x == 0) S.ncand = 0;
         __syncthreads();
         MUX_STAGE(0);
-        if (warp == 0 && lane < kAucWarps) {
+        if (warp == 0) {
+            // tau = the (K+1)-th largest of the 32 half-warp maxima: a lower
+            // bound on the (K+1)-th largest key of the row
             const unsigned long long v = S.wmax[lane];
             int rank = 0;
 #pragma unroll
-            for (int w = 0; w < kAucWarps; ++w) {
+            for (int w = 0; w < 2 * kAucWarps; ++w) {
                 const unsigned long long o = S.wmax[w];
                 rank += (o > v) || (o == v && w < lane);
             }
@@ -1072,7 +1080,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     if (A.eps0 < 1) A.eps0 = 1;
     A.round_guard = 200000000ll;
     const char* cgs = getenv("MUX_CG_SYNC");
-    A.cg_sync = (cgs && *cgs == '1') ? 1 : 0;
+    A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
 
     // shared memory: two row buffers + price/owner mirrors when they fit
     const size_t rows_bytes = 2ull * (size_t)row_bytes;

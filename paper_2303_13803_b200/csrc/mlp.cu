@@ -143,28 +143,52 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
 
     const int64_t tpr = (p.m + kTile - 1) / kTile;
     const int64_t ntiles = (int64_t)p.n * tpr;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // Register prefetch of the next tile's inputs: thread t owns chunks
+    // c = t + 128 * j (j < 8) of the 128 x 8 (row, k-group) chunk grid; the
+    // global loads for tile k+1 are in flight while tile k's MMAs run.
+    float4 qa[8], qb[8];
+    float4 pf = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto prefetch = [&](int64_t tile) {
+        if (tile >= ntiles) return;
         const int32_t u = (int32_t)(tile / tpr);
         const int32_t v0 = (int32_t)(tile % tpr) * kTile;
-        if (tid < kH / 4) reinterpret_cast<float4*>(sP)[tid] = __ldg(reinterpret_cast<const float4*>(p.P + (int64_t)u * kH) + tid);
-        __syncthreads();
-        // ---- h1 = relu(P[u] + Q[v]) -> bf16, chunk c = (row r, k-group kg)
-#pragma unroll 2
-        for (int c = tid; c < kTile * 8; c += kMlpThreads) {
+        if (tid < kH / 4) pf = __ldg(reinterpret_cast<const float4*>(p.P + (int64_t)u * kH) + tid);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = tid + kMlpThreads * j;
             const int r = (c & 7) | ((c >> 6) << 3);
             const int kg = (c >> 3) & 7;
             const int v = v0 + r;
-            uint4 pk = make_uint4(0, 0, 0, 0);
             if (v < p.m) {
                 const float4* q = reinterpret_cast<const float4*>(p.Q + (int64_t)v * kH + kg * 8);
-                const float4 q0 = __ldg(q), q1 = __ldg(q + 1);
-                const float4 p0 = reinterpret_cast<const float4*>(sP + kg * 8)[0];
-                const float4 p1 = reinterpret_cast<const float4*>(sP + kg * 8)[1];
-                pk.x = pack_bf16(fmaxf(p0.x + q0.x, 0.f), fmaxf(p0.y + q0.y, 0.f));
-                pk.y = pack_bf16(fmaxf(p0.z + q0.z, 0.f), fmaxf(p0.w + q0.w, 0.f));
-                pk.z = pack_bf16(fmaxf(p1.x + q1.x, 0.f), fmaxf(p1.y + q1.y, 0.f));
-                pk.w = pack_bf16(fmaxf(p1.z + q1.z, 0.f), fmaxf(p1.w + q1.w, 0.f));
+                qa[j] = __ldg(q);
+                qb[j] = __ldg(q + 1);
+            } else {
+                qa[j] = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);   // relu -> 0
+                qb[j] = qa[j];
             }
+        }
+    };
+    prefetch(blockIdx.x);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int32_t u = (int32_t)(tile / tpr);
+        const int32_t v0 = (int32_t)(tile % tpr) * kTile;
+        if (tid < kH / 4) reinterpret_cast<float4*>(sP)[tid] = pf;
+        __syncthreads();
+        // ---- h1 = relu(P[u] + Q[v]) -> bf16 into the UMMA layout
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = tid + kMlpThreads * j;
+            const int r = (c & 7) | ((c >> 6) << 3);
+            const int kg = (c >> 3) & 7;
+            const float4 p0 = reinterpret_cast<const float4*>(sP + kg * 8)[0];
+            const float4 p1 = reinterpret_cast<const float4*>(sP + kg * 8)[1];
+            const float4 q0 = qa[j], q1 = qb[j];
+            uint4 pk;
+            pk.x = pack_bf16(fmaxf(p0.x + q0.x, 0.f), fmaxf(p0.y + q0.y, 0.f));
+            pk.y = pack_bf16(fmaxf(p0.z + q0.z, 0.f), fmaxf(p0.w + q0.w, 0.f));
+            pk.z = pack_bf16(fmaxf(p1.x + q1.x, 0.f), fmaxf(p1.y + q1.y, 0.f));
+            pk.w = pack_bf16(fmaxf(p1.z + q1.z, 0.f), fmaxf(p1.w + q1.w, 0.f));
             *reinterpret_cast<uint4*>(sA + core_off(r, kg)) = pk;
         }
         fence_async_smem();
@@ -178,27 +202,29 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
                          idesc, ks > 0);
             mma_commit(&mbar);
         }
+        prefetch(tile + gridDim.x);           // next tile's inputs load under the MMAs
         bar_wait(&mbar, phase);
         phase ^= 1;
         tc_fence_after();
         // ---- epilogue 1: +b2, ReLU -> bf16 -> A operand of layer 3 (own row)
         const int row = tid;
 #pragma unroll
-        for (int cb = 0; cb < kH / 16; ++cb) {
-            float acc[16];
-            tmem_ld16(tmem + lane_base + cb * 16, acc);
+        for (int half = 0; half < 2; ++half) {   // two TMEM loads in flight per wait
+            float acc[2][16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) tmem_ld16(tmem + lane_base + (half * 2 + h) * 16, acc[h]);
             tmem_wait_ld();
-            uint4 lo, hi;
-            lo.x = pack_bf16(fmaxf(acc[0] + sb2[cb * 16 + 0], 0.f), fmaxf(acc[1] + sb2[cb * 16 + 1], 0.f));
-            lo.y = pack_bf16(fmaxf(acc[2] + sb2[cb * 16 + 2], 0.f), fmaxf(acc[3] + sb2[cb * 16 + 3], 0.f));
-            lo.z = pack_bf16(fmaxf(acc[4] + sb2[cb * 16 + 4], 0.f), fmaxf(acc[5] + sb2[cb * 16 + 5], 0.f));
-            lo.w = pack_bf16(fmaxf(acc[6] + sb2[cb * 16 + 6], 0.f), fmaxf(acc[7] + sb2[cb * 16 + 7], 0.f));
-            hi.x = pack_bf16(fmaxf(acc[8] + sb2[cb * 16 + 8], 0.f), fmaxf(acc[9] + sb2[cb * 16 + 9], 0.f));
-            hi.y = pack_bf16(fmaxf(acc[10] + sb2[cb * 16 + 10], 0.f), fmaxf(acc[11] + sb2[cb * 16 + 11], 0.f));
-            hi.z = pack_bf16(fmaxf(acc[12] + sb2[cb * 16 + 12], 0.f), fmaxf(acc[13] + sb2[cb * 16 + 13], 0.f));
-            hi.w = pack_bf16(fmaxf(acc[14] + sb2[cb * 16 + 14], 0.f), fmaxf(acc[15] + sb2[cb * 16 + 15], 0.f));
-            *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2)) = lo;
-            *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 1)) = hi;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cb = half * 2 + h;
+                uint32_t w[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    w[t] = pack_bf16(fmaxf(acc[h][2 * t] + sb2[cb * 16 + 2 * t], 0.f),
+                                     fmaxf(acc[h][2 * t + 1] + sb2[cb * 16 + 2 * t + 1], 0.f));
+                *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2)) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+            }
         }
         tc_fence_before();
         fence_async_smem();
@@ -218,12 +244,16 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         // ---- epilogue 2: +b3, ReLU, dot w4 + b4, clamp, store
         float o = p.b4;
 #pragma unroll
-        for (int cb = 0; cb < kH / 16; ++cb) {
-            float acc[16];
-            tmem_ld16(tmem + lane_base + kH + cb * 16, acc);
+        for (int half = 0; half < 2; ++half) {
+            float acc[2][16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) tmem_ld16(tmem + lane_base + kH + (half * 2 + h) * 16, acc[h]);
             tmem_wait_ld();
 #pragma unroll
-            for (int t = 0; t < 16; ++t) o = fmaf(fmaxf(acc[t] + sb3[cb * 16 + t], 0.f), sw4[cb * 16 + t], o);
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int t = 0; t < 16; ++t)
+                    o = fmaf(fmaxf(acc[h][t] + sb3[(half * 2 + h) * 16 + t], 0.f), sw4[(half * 2 + h) * 16 + t], o);
         }
         o = fminf(1.f, fmaxf(0.f, o));
         const int v = v0 + row;
