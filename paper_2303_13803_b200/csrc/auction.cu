@@ -93,6 +93,7 @@ struct AucArgs {
     int64_t SC;          // benefit scale (n + 1)
     int32_t qshift;      // common power of two divided out of every weight
     int32_t cg_sync;     // 1: cooperative-groups grid.sync, 0: custom barrier
+    int32_t keff;        // candidates actually cached (<= kK)
     int64_t eps0;
     int32_t theta;
     int32_t tail_max;
@@ -378,6 +379,7 @@ __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, in
     int32_t b = INT32_MAX;
 #pragma unroll
     for (int k = 0; k < kK; ++k) {
+        if (k >= A.keff) break;
         // fields by value (no address-taking, so w[] stays in registers)
         const long long jw = (k & 2) ? w[k >> 2].y : w[k >> 2].x;
         const int32_t j = (k & 1) ? (int32_t)(jw >> 32) : (int32_t)(jw & 0xffffffffll);
@@ -446,7 +448,7 @@ template <int WT, bool SP>
 __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, const void* row, int32_t i,
                              int64_t eps) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const bool fast = A.n > (kK * 64);    // >= K+1 half-warps hold columns
+    const bool fast = A.n > (A.keff * 64);   // >= K+1 half-warps hold columns
     bool done = false;
     uint64_t tp0 = gtimer();
 #define MUX_STAGE(k) do { if (threadIdx.x == 0) { const uint64_t _t = gtimer(); S.tprof[k] += _t - tp0; tp0 = _t; } } while (0)
@@ -508,7 +510,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
                 const unsigned long long o = S.wmax[w];
                 rank += (o > v) || (o == v && w < lane);
             }
-            if (rank == kK) S.tau = v;
+            if (rank == A.keff) S.tau = v;
         }
         __syncthreads();
         MUX_STAGE(1);
@@ -586,9 +588,9 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
     MUX_STAGE(3);
     if (warp == 0) {
         // cache: lanes 0..K-1 hold ranks 0..K-1, rank K is the threshold
-        const unsigned long long mk = lane <= kK ? S.sel[lane] : kNoKey;
+        const unsigned long long mk = lane <= A.keff ? S.sel[lane] : kNoKey;
         PCache* rec = A.cache + i;
-        if (lane < kK) {
+        if (lane < A.keff) {
             const bool ok = mk != kNoKey;
             const int32_t j = ok ? key_j(A, mk) : -1;
             rec->j[lane] = j;
@@ -601,7 +603,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
             rec->q[lane] = q;
         }
         if (lane == 0) {
-            const unsigned long long k0 = S.sel[0], k1 = S.sel[1], kt = S.sel[kK];
+            const unsigned long long k0 = S.sel[0], k1 = S.sel[1], kt = S.sel[A.keff];
             rec->thr = kt == kNoKey ? kNegInf : key_v(A, kt);
             rec->valid = 1;
             const int32_t jj = key_j(A, k0);
@@ -940,28 +942,46 @@ auction_kernel(AucArgs A) {
     }
 }
 
-// max over the real N x M block (for epsilon0 and overflow checks)
+// max / bitwise-or over the real N x M block (epsilon0, packing check and the
+// common power of two), one grid-stride pass with 16-byte loads
 template <int WT>
 __global__ void max_q_kernel(const void* W, int64_t ldw, int32_t N, int32_t M, AucCounters* cnt) {
+    constexpr int kV = WT == MUX_W_I32 ? 4 : 2;          // elements per 16-byte load
+    const int64_t vpr = ldw / kV;                          // vectors per row
+    const int64_t total = (int64_t)N * vpr;
     long long mx = 0;
     unsigned long long orv = 0;
-    for (int64_t r = blockIdx.y; r < N; r += gridDim.y)
-        for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < M; c += (int64_t)gridDim.x * blockDim.x) {
-            long long q = (WT == MUX_W_I32) ? (long long)static_cast<const int32_t*>(W)[r * ldw + c]
-                                            : static_cast<const int64_t*>(W)[r * ldw + c];
-            mx = q > mx ? q : mx;
-            orv |= (unsigned long long)q;
-            if (q < 0) atomicOr(&cnt->errors, 1u << 8);
+    bool neg = false;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / vpr;
+        const int64_t c0 = (e - r * vpr) * kV;
+        long long q[4] = {0, 0, 0, 0};
+        if (WT == MUX_W_I32) {
+            const int4 v = __ldg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(W) + r * ldw) + (e - r * vpr));
+            q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+        } else {
+            const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(static_cast<const int64_t*>(W) + r * ldw) + (e - r * vpr));
+            q[0] = v.x; q[1] = v.y;
         }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) orv |= __shfl_xor_sync(0xffffffffu, orv, o);
-    if ((threadIdx.x & 31) == 0 && orv) atomicOr(&cnt->or_q, orv);
+        for (int t = 0; t < kV; ++t) {
+            if (c0 + t >= M) continue;
+            mx = q[t] > mx ? q[t] : mx;
+            orv |= (unsigned long long)q[t];
+            neg |= q[t] < 0;
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        long long o2 = __shfl_xor_sync(0xffffffffu, mx, o);
+        const long long o2 = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = o2 > mx ? o2 : mx;
+        orv |= __shfl_xor_sync(0xffffffffu, orv, o);
     }
-    if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(&cnt->max_q, mx);
+    if (__any_sync(0xffffffffu, neg) && (threadIdx.x & 31) == 0) atomicOr(&cnt->errors, 1u << 8);
+    if ((threadIdx.x & 31) == 0) {
+        if (mx > 0) atomicMax(&cnt->max_q, mx);
+        if (orv) atomicOr(&cnt->or_q, orv);
+    }
 }
 
 // col_of_row for real rows (-1 for padding / zero-weight matches) + total
@@ -1056,9 +1076,9 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     MUX_CUDA_TRY(cudaMemsetAsync(A.cache, 0, sizeof(PCache) * (size_t)n_pad, st));
     int64_t launches = 0;
     if (N > 0 && M > 0) {
-        dim3 g((unsigned)std::min<int64_t>((M + 255) / 256, 64), (unsigned)std::min<int64_t>(N, 4096));
-        if (wtype == MUX_W_I32) max_q_kernel<MUX_W_I32><<<g, 256, 0, st>>>(W, ldw, (int32_t)N, (int32_t)M, A.cnt);
-        else max_q_kernel<MUX_W_I64><<<g, 256, 0, st>>>(W, ldw, (int32_t)N, (int32_t)M, A.cnt);
+        const unsigned g = (unsigned)ctx->num_sms * 8;
+        if (wtype == MUX_W_I32) max_q_kernel<MUX_W_I32><<<g, 512, 0, st>>>(W, ldw, (int32_t)N, (int32_t)M, A.cnt);
+        else max_q_kernel<MUX_W_I64><<<g, 512, 0, st>>>(W, ldw, (int32_t)N, (int32_t)M, A.cnt);
         ++launches;
     }
     AucCounters hc;
@@ -1081,6 +1101,10 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.round_guard = 200000000ll;
     const char* cgs = getenv("MUX_CG_SYNC");
     A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
+    const char* ks = getenv("MUX_K");
+    A.keff = (ks && *ks) ? atoi(ks) : kK;
+    if (A.keff < 1) A.keff = 1;
+    if (A.keff > kK) A.keff = kK;
 
     // shared memory: two row buffers + price/owner mirrors when they fit
     const size_t rows_bytes = 2ull * (size_t)row_bytes;

@@ -28,6 +28,9 @@
 namespace mux {
 
 constexpr int kH = 64;              // hidden width
+constexpr int kKp = 80;             // GEMM K: 64 activations + a ones column (bias) padded to 16
+constexpr int kKg = kKp / 8;        // 16-byte k-groups per operand row
+constexpr int kSbo = kKg * 128;     // bytes between 8-row core groups
 constexpr int kTile = 128;          // pairs per MMA tile (UMMA M)
 constexpr int kMlpThreads = 128;    // 4 warps = the 4 TMEM lane quadrants
 constexpr uint32_t kTmemCols = 128;
@@ -35,10 +38,8 @@ constexpr uint32_t kTmemCols = 128;
 struct MlpDev {
     const float* P;          // [n][64] per-row layer-1 partial (incl. b1)
     const float* Q;          // [m][64] per-column layer-1 partial
-    const uint16_t* W2c;     // [64*64] bf16 bits, UMMA core layout
-    const uint16_t* W3c;
-    const float* b2;
-    const float* b3;
+    const uint16_t* W2c;     // [64 x 80] bf16 bits, UMMA core layout, column 64 = b2
+    const uint16_t* W3c;     // same with b3
     const float* w4;
     float b4;
     int32_t n, m;
@@ -104,27 +105,38 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// byte offset of core chunk (row r, k-group kg) in a 128 x 64 K-major tile
+// byte offset of core chunk (row r, k-group kg) in a K-major tile of kKp columns
 __device__ __forceinline__ uint32_t core_off(int r, int kg) {
-    return (uint32_t)((r >> 3) * 1024 + kg * 128 + (r & 7) * 16);
+    return (uint32_t)((r >> 3) * kSbo + kg * 128 + (r & 7) * 16);
+}
+
+// relu(bf16(a), bf16(b)) packed: one cvt + one HMAX2 per pair
+__device__ __forceinline__ uint32_t relu_bf16x2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    h = __hmax2(h, __float2bfloat162_rn(0.f));
+    return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 template <int WT>
 __global__ void __launch_bounds__(kMlpThreads, 4)
 mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
-    __shared__ __align__(1024) unsigned char sA[kTile * kH * 2];      // 16 KB
-    __shared__ __align__(1024) unsigned char sW2[kH * kH * 2];        // 8 KB
-    __shared__ __align__(1024) unsigned char sW3[kH * kH * 2];
-    __shared__ float sP[kH], sb2[kH], sb3[kH], sw4[kH];
+    __shared__ __align__(1024) unsigned char sA[kTile * kKp * 2];     // 20 KB
+    __shared__ __align__(1024) unsigned char sW2[kH * kKp * 2];       // 10 KB
+    __shared__ __align__(1024) unsigned char sW3[kH * kKp * 2];
+    __shared__ __align__(16) float sP[kH];
+    __shared__ __align__(16) float sw4[kH];
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
 
-    for (int e = tid; e < kH * kH / 8; e += kMlpThreads) {
+    for (int e = tid; e < kH * kKp / 8; e += kMlpThreads) {
         reinterpret_cast<uint4*>(sW2)[e] = reinterpret_cast<const uint4*>(p.W2c)[e];
         reinterpret_cast<uint4*>(sW3)[e] = reinterpret_cast<const uint4*>(p.W3c)[e];
     }
-    if (tid < kH) { sb2[tid] = p.b2[tid]; sb3[tid] = p.b3[tid]; sw4[tid] = p.w4[tid]; }
+    if (tid < kH) sw4[tid] = p.w4[tid];
+    // constant bias k-groups of the A operand: column 64 = 1.0, 65..79 = 0
+    *reinterpret_cast<uint4*>(sA + core_off(tid, 8)) = make_uint4(0x3F80u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sA + core_off(tid, 9)) = make_uint4(0u, 0u, 0u, 0u);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(su32(&tmem_base)), "r"(kTmemCols) : "memory");
@@ -169,6 +181,16 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
             }
         }
     };
+    auto issue_layer = [&](uint32_t dcol, uint32_t b_addr) {
+        if (tid == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int ks = 0; ks < kKp / 16; ++ks)
+                mma_bf16(tmem + dcol, umma_desc(a_addr + ks * 256, 128, kSbo), umma_desc(b_addr + ks * 256, 128, kSbo),
+                         idesc, ks > 0);
+            mma_commit(&mbar);
+        }
+    };
     prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int32_t u = (int32_t)(tile / tpr);
@@ -185,28 +207,21 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
             const float4 p1 = reinterpret_cast<const float4*>(sP + kg * 8)[1];
             const float4 q0 = qa[j], q1 = qb[j];
             uint4 pk;
-            pk.x = pack_bf16(fmaxf(p0.x + q0.x, 0.f), fmaxf(p0.y + q0.y, 0.f));
-            pk.y = pack_bf16(fmaxf(p0.z + q0.z, 0.f), fmaxf(p0.w + q0.w, 0.f));
-            pk.z = pack_bf16(fmaxf(p1.x + q1.x, 0.f), fmaxf(p1.y + q1.y, 0.f));
-            pk.w = pack_bf16(fmaxf(p1.z + q1.z, 0.f), fmaxf(p1.w + q1.w, 0.f));
+            pk.x = relu_bf16x2(p0.x + q0.x, p0.y + q0.y);
+            pk.y = relu_bf16x2(p0.z + q0.z, p0.w + q0.w);
+            pk.z = relu_bf16x2(p1.x + q1.x, p1.y + q1.y);
+            pk.w = relu_bf16x2(p1.z + q1.z, p1.w + q1.w);
             *reinterpret_cast<uint4*>(sA + core_off(r, kg)) = pk;
         }
         fence_async_smem();
         __syncthreads();
-        // ---- layer 2 on the tensor cores
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int ks = 0; ks < kH / 16; ++ks)
-                mma_bf16(tmem, umma_desc(a_addr + ks * 256, 128, 1024), umma_desc(w2_addr + ks * 256, 128, 1024),
-                         idesc, ks > 0);
-            mma_commit(&mbar);
-        }
+        // ---- layer 2 (bias in the ones column) on the tensor cores
+        issue_layer(0, w2_addr);
         prefetch(tile + gridDim.x);           // next tile's inputs load under the MMAs
         bar_wait(&mbar, phase);
         phase ^= 1;
         tc_fence_after();
-        // ---- epilogue 1: +b2, ReLU -> bf16 -> A operand of layer 3 (own row)
+        // ---- epilogue 1: ReLU -> bf16 -> A operand of layer 3 (own row)
         const int row = tid;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {   // two TMEM loads in flight per wait
@@ -219,9 +234,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
                 const int cb = half * 2 + h;
                 uint32_t w[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    w[t] = pack_bf16(fmaxf(acc[h][2 * t] + sb2[cb * 16 + 2 * t], 0.f),
-                                     fmaxf(acc[h][2 * t + 1] + sb2[cb * 16 + 2 * t + 1], 0.f));
+                for (int t = 0; t < 8; ++t) w[t] = relu_bf16x2(acc[h][2 * t], acc[h][2 * t + 1]);
                 *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2)) = make_uint4(w[0], w[1], w[2], w[3]);
                 *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
             }
@@ -230,18 +243,11 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         fence_async_smem();
         __syncthreads();
         // ---- layer 3 on the tensor cores
-        if (tid == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int ks = 0; ks < kH / 16; ++ks)
-                mma_bf16(tmem + kH, umma_desc(a_addr + ks * 256, 128, 1024), umma_desc(w3_addr + ks * 256, 128, 1024),
-                         idesc, ks > 0);
-            mma_commit(&mbar);
-        }
+        issue_layer(kH, w3_addr);
         bar_wait(&mbar, phase);
         phase ^= 1;
         tc_fence_after();
-        // ---- epilogue 2: +b3, ReLU, dot w4 + b4, clamp, store
+        // ---- epilogue 2: ReLU, dot w4 + b4, clamp, store
         float o = p.b4;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
@@ -252,8 +258,13 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int t = 0; t < 16; ++t)
-                    o = fmaf(fmaxf(acc[h][t] + sb3[(half * 2 + h) * 16 + t], 0.f), sw4[(half * 2 + h) * 16 + t], o);
+                for (int t4 = 0; t4 < 4; ++t4) {
+                    const float4 w4 = reinterpret_cast<const float4*>(sw4 + (half * 2 + h) * 16)[t4];
+                    o = fmaf(fmaxf(acc[h][4 * t4 + 0], 0.f), w4.x, o);
+                    o = fmaf(fmaxf(acc[h][4 * t4 + 1], 0.f), w4.y, o);
+                    o = fmaf(fmaxf(acc[h][4 * t4 + 2], 0.f), w4.z, o);
+                    o = fmaf(fmaxf(acc[h][4 * t4 + 3], 0.f), w4.w, o);
+                }
         }
         o = fminf(1.f, fmaxf(0.f, o));
         const int v = v0 + row;
@@ -319,12 +330,14 @@ static uint16_t bf16_bits(float f) {
     return (uint16_t)(x >> 16);
 }
 
-// W [64 out][64 in] row-major -> UMMA K-major core layout (B operand, N = out)
-static void to_core_layout(const float* W, uint16_t* dst) {
+// W [64 out][64 in] row-major + bias -> UMMA K-major core layout of the
+// [64 x 80] B operand (column 64 = bias, 65..79 = 0), N = out
+static void to_core_layout(const float* W, const float* bias, uint16_t* dst) {
     for (int nn = 0; nn < kH; ++nn)
-        for (int k = 0; k < kH; ++k) {
-            const size_t off = (size_t)(nn >> 3) * 512 + (size_t)(k >> 3) * 64 + (size_t)(nn & 7) * 8 + (k & 7);
-            dst[off] = bf16_bits(W[nn * kH + k]);
+        for (int k = 0; k < kKp; ++k) {
+            const float val = k < kH ? W[nn * kH + k] : (k == kH ? bias[nn] : 0.f);
+            const size_t off = (size_t)(nn >> 3) * (kSbo / 2) + (size_t)(k >> 3) * 64 + (size_t)(nn & 7) * 8 + (k & 7);
+            dst[off] = bf16_bits(val);
         }
 }
 
@@ -333,13 +346,10 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
                        cudaStream_t st, int64_t* launches) {
     if (w->hidden != kH) { set_error("mux_score_mlp: hidden width must be 64"); return MUX_EINVAL; }
     // parameter block on device: W2c, W3c (bf16 core layout), b2, b3, w4
-    const size_t o_w2 = 0, o_w3 = o_w2 + kH * kH * 2, o_b2 = o_w3 + kH * kH * 2, o_b3 = o_b2 + kH * 4,
-                 o_w4 = o_b3 + kH * 4, o_end = o_w4 + kH * 4;
+    const size_t o_w2 = 0, o_w3 = o_w2 + kH * kKp * 2, o_w4 = o_w3 + kH * kKp * 2, o_end = o_w4 + kH * 4;
     std::string blob(o_end, '\0');
-    to_core_layout(w->W2, reinterpret_cast<uint16_t*>(&blob[o_w2]));
-    to_core_layout(w->W3, reinterpret_cast<uint16_t*>(&blob[o_w3]));
-    memcpy(&blob[o_b2], w->b2, kH * 4);
-    memcpy(&blob[o_b3], w->b3, kH * 4);
+    to_core_layout(w->W2, w->b2, reinterpret_cast<uint16_t*>(&blob[o_w2]));
+    to_core_layout(w->W3, w->b3, reinterpret_cast<uint16_t*>(&blob[o_w3]));
     memcpy(&blob[o_w4], w->w4, kH * 4);
     const size_t pq_bytes = sizeof(float) * kH * (size_t)(n + m);
     MUX_TRY(ctx->mlp.ensure(o_end + 256 + pq_bytes));
@@ -361,8 +371,6 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
     p.P = P; p.Q = Q;
     p.W2c = reinterpret_cast<const uint16_t*>(base + o_w2);
     p.W3c = reinterpret_cast<const uint16_t*>(base + o_w3);
-    p.b2 = reinterpret_cast<const float*>(base + o_b2);
-    p.b3 = reinterpret_cast<const float*>(base + o_b3);
     p.w4 = reinterpret_cast<const float*>(base + o_w4);
     p.b4 = w->b4;
     p.n = (int32_t)n; p.m = (int32_t)m;

@@ -24,7 +24,8 @@ def bf16(x):
 
 
 def emulated(params, on, share, off):
-    """Kernel-precision forward: P/Q fp32, h1/W2/h2/W3 bf16, fp32 accumulate."""
+    """Kernel-precision forward: P/Q fp32, h1/W2/h2/W3 and the layer-2/3
+    biases bf16 (they ride in the GEMM as a ones column), fp32 accumulate."""
     f32 = np.float32
     W1 = params["W1"].astype(f32)
     shift, scale = params["shift"].astype(f32), params["scale"].astype(f32)
@@ -37,8 +38,8 @@ def emulated(params, on, share, off):
     out = np.empty((P.shape[0], Q.shape[0]), dtype=np.float64)
     for u in range(P.shape[0]):
         h1 = bf16(np.maximum(P[u][None, :] + Q, 0))
-        h2 = bf16(np.maximum(h1 @ W2.T + params["b2"].astype(f32), 0))
-        h3 = np.maximum(h2 @ W3.T + params["b3"].astype(f32), 0)
+        h2 = bf16(np.maximum(h1 @ W2.T + bf16(params["b2"]), 0))
+        h3 = np.maximum(h2 @ W3.T + bf16(params["b3"]), 0)
         out[u] = np.clip(h3 @ params["w4"].astype(f32) + f32(params["b4"]), 0, 1)
     return out
 
