@@ -65,7 +65,10 @@ struct AucCounters {
     unsigned long long rounds, bids, scans, tail_bids, phases, hits;
     long long ns_total, ns_tail, ns_tail_hit, ns_tail_scan, ns_tail_wait, ns_a1, ns_a2, ns_b;
     unsigned long long tail_scans;
-    long long ns_stage[5];
+    long long cyc_hitloop;
+    long long cyc_fetch;
+    unsigned long long tail_hits;
+    long long ns_stage[6];
     long long max_q;
     long long total_q;
     unsigned long long or_q;
@@ -299,6 +302,10 @@ __device__ __forceinline__ void grid_barrier(const AucArgs& A, cg::grid_group& g
 // ---- per-CTA shared state ------------------------------------------------------
 
 struct Shared {
+    PCache rec[2];                           // prefetched cache records (tail)
+    uint64_t rbar[2];                        // record-buffer mbarriers
+    uint32_t rbar_phase[2];
+    int32_t rec_person[2];
     uint64_t bar[2];                         // row-buffer mbarriers
     uint32_t bar_phase[2];
     int32_t row_person[2];                   // person whose row sits in buffer b (-1 none)
@@ -313,7 +320,7 @@ struct Shared {
     unsigned long long sel[kK + 1];            // selected top-(K+1) keys
     int32_t ncand;
     unsigned long long cand[kCandMax];          // keys >= tau
-    unsigned long long tprof[8];                 // tail stage timers (ns)
+    unsigned long long tprof[8];                 // scan stage timers (SM cycles); [7] = scans
 };
 
 struct Dyn {             // carve-up of dynamic shared memory
@@ -349,6 +356,22 @@ __device__ __forceinline__ void fetch_row(const AucArgs& A, Shared& S, Dyn& D, i
     const char* src = static_cast<const char*>(A.W) + (size_t)i * A.ldw * esz;
     tma_row(&S.bar[b], D.row(b), src, (uint32_t)A.row_bytes);
 }
+// Prefetch person i's cache record into S.rec[b] (thread 0; tail only).
+__device__ __forceinline__ void fetch_rec(const AucArgs& A, Shared& S, int b, int32_t i) {
+    if (S.rec_person[b] >= 0) { mbar_wait(&S.rbar[b], S.rbar_phase[b]); S.rbar_phase[b] ^= 1u; }
+    S.rec_person[b] = i;
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy cache stores -> TMA reads
+    tma_row(&S.rbar[b], &S.rec[b], A.cache + i, (uint32_t)sizeof(PCache));
+}
+// Claim the prefetched record of person i if buffer b holds it (thread 0).
+__device__ __forceinline__ const PCache* claim_rec(Shared& S, int b, int32_t i) {
+    if (S.rec_person[b] != i) return nullptr;
+    mbar_wait(&S.rbar[b], S.rbar_phase[b]);
+    S.rbar_phase[b] ^= 1u;
+    S.rec_person[b] = -1;
+    return &S.rec[b];
+}
+
 // Wait for buffer b (all threads); returns the row pointer.
 template <int WT>
 __device__ __forceinline__ const void* wait_row(const AucArgs& A, Shared& S, Dyn& D, int b, int32_t i) {
@@ -367,11 +390,16 @@ __device__ __forceinline__ int64_t bid_from(int64_t a1, int64_t v1, int64_t seco
 // hit; ties on value go to the lower object index, like a full scan.
 template <bool SP>
 __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, int32_t i, int64_t eps,
-                                          int32_t& j1, int64_t& bid) {
+                                          int32_t& j1, int64_t& bid, const PCache* srec = nullptr) {
     const longlong2* rec = reinterpret_cast<const longlong2*>(A.cache + i);
     longlong2 w[13];     // j[0..16) | q[0..16) | thr, valid
+    if (srec) {          // prefetched copy in shared memory
 #pragma unroll
-    for (int t = 0; t < 13; ++t) w[t] = __ldcg(rec + t);
+        for (int t = 0; t < 13; ++t) w[t] = reinterpret_cast<const longlong2*>(srec)[t];
+    } else {
+#pragma unroll
+        for (int t = 0; t < 13; ++t) w[t] = __ldcg(rec + t);
+    }
     const int32_t valid = (int32_t)(w[12].y & 0xffffffffll);
     if (!valid) return false;
     const int64_t thr = w[12].x;
@@ -450,8 +478,8 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool fast = A.n > (A.keff * 64);   // >= K+1 half-warps hold columns
     bool done = false;
-    uint64_t tp0 = gtimer();
-#define MUX_STAGE(k) do { if (threadIdx.x == 0) { const uint64_t _t = gtimer(); S.tprof[k] += _t - tp0; tp0 = _t; } } while (0)
+    uint64_t tp0 = clock64();
+#define MUX_STAGE(k) do { if (threadIdx.x == 0) { const uint64_t _t = clock64(); S.tprof[k] += _t - tp0; tp0 = _t; } } while (0)
     if (fast) {
         // pass 1: per-thread best (value, lowest index) and per-group maxima.
         // kIters fixed-trip steps keep the group maxima in registers; rows
@@ -553,7 +581,17 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
         __syncthreads();
         MUX_STAGE(2);
         const int nc = S.ncand;
-        if (nc <= kCandMax) {
+        if (nc <= 32) {
+            if (warp == 0) {
+                const unsigned long long key = lane < nc ? S.cand[lane] : kNoKey;
+                int rank = 0;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) rank += __shfl_sync(0xffffffffu, key, e) > key;
+                if (lane < nc && rank <= kK) S.sel[rank] = key;
+                if (lane <= kK && lane >= nc) S.sel[lane] = kNoKey;
+            }
+            done = true;
+        } else if (nc <= kCandMax) {
             for (int t = threadIdx.x; t < nc; t += kAucThreads) {
                 const unsigned long long key = S.cand[t];
                 int rank = 0;
@@ -615,6 +653,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
     }
     __syncthreads();
     MUX_STAGE(4);
+    if (threadIdx.x == 0) S.tprof[7] += 1;
 #undef MUX_STAGE
 }
 
@@ -672,19 +711,22 @@ __device__ void tail_gs(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_
     __syncthreads();
     unsigned long long steps = 0, scans = 0, hits = 0;
     uint64_t ns_hit = 0, ns_scan = 0, ns_wait = 0;
+    uint64_t cyc_hitloop = 0, cyc_steps = 0;
     int cur_buf = 0;
     for (;;) {
         const uint64_t th0 = gtimer();
         // warp 0 runs every cache-hit step alone (no CTA barrier); it stops at
         // the first miss and hands that person to the whole CTA.
         if (threadIdx.x == 0) {
+            const uint64_t c0 = clock64();
             int32_t need = -1;
             int32_t top = S.top;
             while (top > 0 && steps <= (unsigned long long)A.round_guard) {
                 const int32_t i = S.stack[top - 1];
                 int32_t j1 = 0;
                 int64_t bid = 0;
-                if (!cache_bid<SP>(A, P, i, eps, j1, bid)) { need = i; break; }
+                const PCache* srec = SP ? claim_rec(S, cur_buf, i) : nullptr;
+                if (!cache_bid<SP>(A, P, i, eps, j1, bid, srec)) { need = i; break; }
                 const int32_t prev = gs_assign<SP>(A, D, i, j1, bid);
                 --top;
                 if (prev >= 0) S.stack[top++] = prev;
@@ -693,7 +735,10 @@ __device__ void tail_gs(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_
             }
             S.top = top;
             S.scan_i = steps > (unsigned long long)A.round_guard ? -2 : need;
+            const uint64_t c1 = clock64();
+            cyc_hitloop += c1 - c0;
             if (need >= 0 && SP && S.row_person[cur_buf] != need) fetch_row<WT>(A, S, D, cur_buf, need);
+            cyc_steps += clock64() - c1;
         }
         __syncthreads();
         const uint64_t th1 = gtimer();
@@ -711,8 +756,11 @@ __device__ void tail_gs(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_
             int32_t t2 = S.top - 1;
             if (prev >= 0) {
                 S.stack[t2++] = prev;
-                // prefetch the displaced person's row: it bids next
-                if (SP) fetch_row<WT>(A, S, D, cur_buf ^ 1, prev);
+                // prefetch the displaced person's row and cache record: it bids next
+                if (SP) {
+                    fetch_row<WT>(A, S, D, cur_buf ^ 1, prev);
+                    fetch_rec(A, S, cur_buf ^ 1, prev);
+                }
             }
             S.top = t2;
         }
@@ -724,13 +772,21 @@ __device__ void tail_gs(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_
     }
     if (S.scan_i == -2 && threadIdx.x == 0) atomicOr(&A.cnt->errors, kErrIterGuard);
     // drain a pending prefetch so the mbarrier phases stay consistent
-    if (SP && threadIdx.x == 0) { drain_row(A, S, 0); drain_row(A, S, 1); }
+    if (SP && threadIdx.x == 0) {
+        drain_row(A, S, 0);
+        drain_row(A, S, 1);
+        for (int b = 0; b < 2; ++b)
+            if (S.rec_person[b] >= 0) { mbar_wait(&S.rbar[b], S.rbar_phase[b]); S.rbar_phase[b] ^= 1u; S.rec_person[b] = -1; }
+    }
     if (threadIdx.x == 0) {
         atomicAdd(&A.cnt->tail_bids, steps);
         atomicAdd(&A.cnt->bids, steps);
         atomicAdd(&A.cnt->scans, scans);
         atomicAdd(&A.cnt->hits, hits);
         atomicAdd(&A.cnt->tail_scans, scans);
+        atomicAdd((unsigned long long*)&A.cnt->cyc_hitloop, (unsigned long long)cyc_hitloop);
+        atomicAdd((unsigned long long*)&A.cnt->cyc_fetch, (unsigned long long)cyc_steps);
+        atomicAdd((unsigned long long*)&A.cnt->tail_hits, hits);
         atomicAdd((unsigned long long*)&A.cnt->ns_tail_hit, (unsigned long long)ns_hit);
         atomicAdd((unsigned long long*)&A.cnt->ns_tail_scan, (unsigned long long)ns_scan);
         atomicAdd((unsigned long long*)&A.cnt->ns_tail_wait, (unsigned long long)ns_wait);
@@ -762,7 +818,11 @@ auction_kernel(AucArgs A) {
     if (threadIdx.x == 0) {
         mbar_init(&S.bar[0], 1);
         mbar_init(&S.bar[1], 1);
+        mbar_init(&S.rbar[0], 1);
+        mbar_init(&S.rbar[1], 1);
         fence_mbar_init();
+        S.rbar_phase[0] = S.rbar_phase[1] = 0;
+        S.rec_person[0] = S.rec_person[1] = -1;
         S.bar_phase[0] = S.bar_phase[1] = 0;
         S.row_person[0] = S.row_person[1] = -1;
         for (int k = 0; k < 8; ++k) S.tprof[k] = 0;
@@ -936,6 +996,7 @@ auction_kernel(AucArgs A) {
         A.cnt->ns_total = (long long)(gtimer() - t_start);
         A.cnt->ns_tail = (long long)t_tail;
         for (int k = 0; k < 5; ++k) A.cnt->ns_stage[k] = (long long)S.tprof[k];
+        A.cnt->ns_stage[5] = (long long)S.tprof[7];
         A.cnt->ns_a1 = (long long)t_a1;
         A.cnt->ns_a2 = (long long)t_a2;
         A.cnt->ns_b = (long long)t_b;
@@ -1156,13 +1217,17 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         stats->cache_hits = (int64_t)hc.hits;
         stats->launches += launches;
         if (getenv("MUX_VERBOSE"))
+            fprintf(stderr, "[mux] tail: hits %llu hit-loop cycles/hit %.0f; fetch cycles/scan %.0f\n", hc.tail_hits,
+                    hc.cyc_hitloop / (double)(hc.tail_hits + 1), hc.cyc_fetch / (double)(hc.tail_scans + 1));
+        if (getenv("MUX_VERBOSE"))
             fprintf(stderr, "[mux] tail: scans %llu hit_ms %.2f scan_ms %.2f wait_ms %.2f | rounds: a1 %.2f a2 %.2f b %.2f ms\n",
                     hc.tail_scans, hc.ns_tail_hit * 1e-6, hc.ns_tail_scan * 1e-6, hc.ns_tail_wait * 1e-6,
                     hc.ns_a1 * 1e-6, hc.ns_a2 * 1e-6, hc.ns_b * 1e-6);
         if (getenv("MUX_VERBOSE"))
-            fprintf(stderr, "[mux] CTA0 scan stages ms: pass1 %.2f tau %.2f pass2 %.2f rank %.2f store %.2f\n",
-                    hc.ns_stage[0] * 1e-6, hc.ns_stage[1] * 1e-6, hc.ns_stage[2] * 1e-6, hc.ns_stage[3] * 1e-6,
-                    hc.ns_stage[4] * 1e-6);
+            fprintf(stderr, "[mux] CTA0 scans %lld, cycles/scan: pass1 %.0f tau %.0f pass2 %.0f rank %.0f store %.0f\n",
+                    hc.ns_stage[5], hc.ns_stage[0] / (double)(hc.ns_stage[5] + 1), hc.ns_stage[1] / (double)(hc.ns_stage[5] + 1),
+                    hc.ns_stage[2] / (double)(hc.ns_stage[5] + 1), hc.ns_stage[3] / (double)(hc.ns_stage[5] + 1),
+                    hc.ns_stage[4] / (double)(hc.ns_stage[5] + 1));
     }
     return MUX_OK;
 }

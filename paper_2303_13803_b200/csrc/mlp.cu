@@ -30,10 +30,12 @@ namespace mux {
 constexpr int kH = 64;              // hidden width
 constexpr int kKp = 80;             // GEMM K: 64 activations + a ones column (bias) padded to 16
 constexpr int kKg = kKp / 8;        // 16-byte k-groups per operand row
-constexpr int kSbo = kKg * 128;     // bytes between 8-row core groups
+constexpr int kSbo = kKg * 128;     // bytes between 8-row core groups (B operands)
+constexpr int kSboA = kSbo + 16;    // A operand: +16 B per group rotates banks (conflict-free epilogue stores)
 constexpr int kTile = 128;          // pairs per MMA tile (UMMA M)
 constexpr int kMlpThreads = 128;    // 4 warps = the 4 TMEM lane quadrants
-constexpr uint32_t kTmemCols = 128;
+constexpr int kMlpCtasPerSm = 4;
+constexpr uint32_t kTmemCols = 64;  // one accumulator reused by layers 2 and 3
 
 struct MlpDev {
     const float* P;          // [n][64] per-row layer-1 partial (incl. b1)
@@ -105,9 +107,9 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// byte offset of core chunk (row r, k-group kg) in a K-major tile of kKp columns
+// byte offset of core chunk (row r, k-group kg) in the A tile (K-major, kKp columns)
 __device__ __forceinline__ uint32_t core_off(int r, int kg) {
-    return (uint32_t)((r >> 3) * kSbo + kg * 128 + (r & 7) * 16);
+    return (uint32_t)((r >> 3) * kSboA + kg * 128 + (r & 7) * 16);
 }
 
 // relu(bf16(a), bf16(b)) packed: one cvt + one HMAX2 per pair
@@ -118,9 +120,9 @@ __device__ __forceinline__ uint32_t relu_bf16x2(float a, float b) {
 }
 
 template <int WT>
-__global__ void __launch_bounds__(kMlpThreads, 4)
+__global__ void __launch_bounds__(kMlpThreads, kMlpCtasPerSm)
 mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
-    __shared__ __align__(1024) unsigned char sA[kTile * kKp * 2];     // 20 KB
+    __shared__ __align__(1024) unsigned char sA[(kTile / 8) * kSboA];  // ~20 KB
     __shared__ __align__(1024) unsigned char sW2[kH * kKp * 2];       // 10 KB
     __shared__ __align__(1024) unsigned char sW3[kH * kKp * 2];
     __shared__ __align__(16) float sP[kH];
@@ -186,7 +188,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
             tc_fence_after();
 #pragma unroll
             for (int ks = 0; ks < kKp / 16; ++ks)
-                mma_bf16(tmem + dcol, umma_desc(a_addr + ks * 256, 128, kSbo), umma_desc(b_addr + ks * 256, 128, kSbo),
+                mma_bf16(tmem + dcol, umma_desc(a_addr + ks * 256, 128, kSboA), umma_desc(b_addr + ks * 256, 128, kSbo),
                          idesc, ks > 0);
             mma_commit(&mbar);
         }
@@ -197,14 +199,16 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         const int32_t v0 = (int32_t)(tile % tpr) * kTile;
         if (tid < kH / 4) reinterpret_cast<float4*>(sP)[tid] = pf;
         __syncthreads();
-        // ---- h1 = relu(P[u] + Q[v]) -> bf16 into the UMMA layout
+        // ---- h1 = relu(P[u] + Q[v]) -> bf16 into the UMMA layout.  A thread's
+        // chunks c = tid + 128 j all share k-group (tid >> 3) & 7: P loads once.
+        const int kg_t = (tid >> 3) & 7;
+        const float4 p0 = reinterpret_cast<const float4*>(sP + kg_t * 8)[0];
+        const float4 p1 = reinterpret_cast<const float4*>(sP + kg_t * 8)[1];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int c = tid + kMlpThreads * j;
             const int r = (c & 7) | ((c >> 6) << 3);
-            const int kg = (c >> 3) & 7;
-            const float4 p0 = reinterpret_cast<const float4*>(sP + kg * 8)[0];
-            const float4 p1 = reinterpret_cast<const float4*>(sP + kg * 8)[1];
+            const int kg = kg_t;
             const float4 q0 = qa[j], q1 = qb[j];
             uint4 pk;
             pk.x = relu_bf16x2(p0.x + q0.x, p0.y + q0.y);
@@ -243,7 +247,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         fence_async_smem();
         __syncthreads();
         // ---- layer 3 on the tensor cores
-        issue_layer(kH, w3_addr);
+        issue_layer(0, w3_addr);
         bar_wait(&mbar, phase);
         phase ^= 1;
         tc_fence_after();
@@ -253,7 +257,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         for (int half = 0; half < 2; ++half) {
             float acc[2][16];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) tmem_ld16(tmem + lane_base + kH + (half * 2 + h) * 16, acc[h]);
+            for (int h = 0; h < 2; ++h) tmem_ld16(tmem + lane_base + (half * 2 + h) * 16, acc[h]);
             tmem_wait_ld();
 #pragma unroll
             for (int h = 0; h < 2; ++h)
@@ -376,7 +380,7 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
     p.n = (int32_t)n; p.m = (int32_t)m;
     const int64_t tiles = n * ((m + kTile - 1) / kTile);
     if (tiles > 0) {
-        const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * 4);
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * kMlpCtasPerSm);
         const double qscale = ldexp(1.0, qbits);
         if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
         else mlp_pairs_kernel<MUX_W_I32><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
