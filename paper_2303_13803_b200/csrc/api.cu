@@ -176,7 +176,7 @@ int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t 
     }
     if (stats) memset(stats, 0, sizeof(*stats));
     MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", 16)));
+                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1)));
     if (out_on_host && n > 0) {
         MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));
@@ -225,7 +225,7 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)n));
     int32_t* col_dev = ctx->colout.as<int32_t>();
     MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, MUX_W_I32, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", 16)));
+                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1)));
     MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_host, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     if (stats) {

@@ -48,7 +48,7 @@ namespace mux {
 constexpr int kK = 15;                // cached candidates per person (K + 1 = 16)
 constexpr int kAucThreads = 512;      // 16 warps per CTA
 constexpr int kAucWarps = kAucThreads / kWarp;
-constexpr int kTailMax = 64;          // largest tail handled by the single CTA
+constexpr int kTailMax = 256;         // largest tail handed to the tail modes
 constexpr int64_t kNegInf = INT64_MIN / 4;
 constexpr unsigned long long kNoKey = 0ull;
 constexpr size_t kSmemBudget = 220 * 1024;
@@ -62,6 +62,9 @@ struct AucCounters {
     uint32_t tail_epoch;
     uint32_t bar_count;                 // custom grid barrier
     uint32_t bar_gen;
+    int32_t qhead;                      // async tail: next queued person
+    int32_t free_count;                 // async tail: chains still open
+    unsigned long long async_fail;      // async tail: rejected bids
     unsigned long long rounds, bids, scans, tail_bids, phases, hits;
     long long ns_total, ns_tail, ns_tail_hit, ns_tail_scan, ns_tail_wait, ns_a1, ns_a2, ns_b;
     unsigned long long tail_scans;
@@ -97,6 +100,7 @@ struct AucArgs {
     int32_t qshift;      // common power of two divided out of every weight
     int32_t cg_sync;     // 1: cooperative-groups grid.sync, 0: custom barrier
     int32_t keff;        // candidates actually cached (<= kK)
+    int32_t async_tail;  // 1: tail chains run concurrently on many CTAs
     int64_t eps0;
     int32_t theta;
     int32_t tail_max;
@@ -111,6 +115,7 @@ struct AucArgs {
     int32_t* bidj;       // [n_pad]
     unsigned long long* bidpk;  // [n_pad]
     PCache* cache;       // [n_pad]
+    unsigned long long* word;   // [n_pad] async tail state: price << idbits | (idmask - owner), 0 = unowned
     AucCounters* cnt;
     int32_t n_pad;
     int32_t row_bytes;   // bytes of one staged weight row (multiple of 16)
@@ -312,6 +317,7 @@ struct Shared {
     int32_t stack[kTailMax + 1];
     int32_t top;
     int32_t scan_i;                          // tail: person needing a scan (-1 = done)
+    int32_t chain_i;                         // async tail: person at the head of this CTA's chain
     int32_t j1;
     int64_t bid;
     unsigned long long wk[kAucWarps][kK + 1];  // per-warp merged keys (slow path)
@@ -795,6 +801,154 @@ __device__ void tail_gs(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_
     __syncthreads();
 }
 
+// ---- asynchronous multi-CTA tail -----------------------------------------------
+//
+// The few persons left at the end of a phase each start a displacement chain
+// (bid, displace the owner, the displaced person bids next, ... until a free
+// object is taken).  The Gauss-Seidel tail runs these chains one after
+// another; here every CTA takes a chain from a queue and runs it concurrently.
+// Ownership and prices live in one 64-bit word per object,
+// price << idbits | (idmask - owner), and a bid is committed with atomicMax:
+// it wins iff its price is higher than the current one.  A bid computed from a
+// stale (lower) price snapshot is still a valid epsilon-CS bid when it wins
+// (stale prices only over-estimate the second-best value), so each CTA bids
+// from its own shared-memory price mirror and refreshes an entry when a bid is
+// rejected.  The result is an optimal assignment; which of several tied optima
+// is returned may vary between runs, so the mode is used for large problems
+// only (deterministic Gauss-Seidel tail otherwise).
+
+__device__ __forceinline__ unsigned long long pack_state(const AucArgs& A, int64_t price, int32_t owner) {
+    return ((unsigned long long)price << A.idbits) | (owner >= 0 ? A.idmask - (unsigned long long)owner : 0ull);
+}
+
+// Commit person i's bid on j1 (thread 0).  Returns -2 if rejected (the mirror
+// entry is refreshed), -1 if the chain ended on a free object, else the
+// displaced person.
+template <bool SP>
+__device__ __forceinline__ int32_t async_commit(const AucArgs& A, Dyn& D, int32_t i, int32_t j1, int64_t bid) {
+    check_bid(A, bid);
+    const unsigned long long pk = pack_state(A, bid, i);
+    const unsigned long long old = atomicMax(A.word + j1, pk);
+    if (pk <= old) {
+        if (SP) D.price[j1] = (int64_t)(old >> A.idbits);
+        atomicAdd(&A.cnt->async_fail, 1ull);
+        return -2;
+    }
+    if (SP) D.price[j1] = bid;
+    A.col[i] = j1;
+    const unsigned long long low = old & A.idmask;
+    if (low == 0) return -1;
+    const int32_t prev = (int32_t)(A.idmask - low);
+    A.col[prev] = -1;
+    return prev;
+}
+
+__device__ __forceinline__ void stage_word_prices(const AucArgs& A, int64_t* sp) {
+    for (int t = threadIdx.x; t < A.n_pad; t += blockDim.x) sp[t] = (int64_t)(__ldcg(A.word + t) >> A.idbits);
+}
+
+template <int WT, bool SP>
+__device__ void tail_async(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_t count, const int32_t* src,
+                           cg::grid_group& grid) {
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = gtid; t < A.n_pad; t += gsize)
+        A.word[t] = t < A.n ? pack_state(A, __ldcg(A.price + t), __ldcg(A.owner + t)) : 0ull;
+    if (gtid == 0) {
+        A.cnt->qhead = 0;
+        A.cnt->free_count = count;
+    }
+    grid_barrier(A, grid);
+    const int64_t* P = D.price;
+    unsigned long long steps = 0, scans = 0, hits = 0;
+    int cur_buf = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const int32_t idx = atomicAdd(&A.cnt->qhead, 1);
+            S.chain_i = idx < count ? __ldcg(src + idx) : -1;
+        }
+        __syncthreads();
+        if (S.chain_i < 0) break;
+        stage_word_prices(A, D.price);
+        __syncthreads();
+        for (;;) {
+            if (threadIdx.x == 0) {
+                int32_t cur = S.chain_i;
+                int32_t need = -1;
+                int fails = 0;
+                while (cur >= 0) {
+                    int32_t j1 = 0;
+                    int64_t bid = 0;
+                    const PCache* srec = claim_rec(S, cur_buf, cur);
+                    if (!cache_bid<SP>(A, P, cur, eps, j1, bid, srec)) { need = cur; break; }
+                    const int32_t r = async_commit<SP>(A, D, cur, j1, bid);
+                    ++steps;
+                    if (r == -2) { ++fails; continue; }
+                    ++hits;
+                    if (r == -1) { atomicSub(&A.cnt->free_count, 1); cur = -1; break; }
+                    cur = r;
+                }
+                S.chain_i = cur;
+                S.scan_i = need;
+                if (need >= 0 && S.row_person[cur_buf] != need) fetch_row<WT>(A, S, D, cur_buf, need);
+            }
+            __syncthreads();
+            const int32_t i = S.scan_i;
+            if (i < 0) break;                      // chain finished
+            const void* row = wait_row<WT>(A, S, D, cur_buf, i);
+            cta_scan_bid<WT, SP>(A, S, P, row, i, eps);
+            if (threadIdx.x == 0) {
+                if (i < A.N && A.M > 0) S.bar_phase[cur_buf] ^= 1u;
+                S.row_person[cur_buf] = -1;
+                const int32_t r = async_commit<SP>(A, D, i, S.j1, S.bid);
+                ++steps;
+                ++scans;
+                if (r == -2) {
+                    S.chain_i = i;                 // rejected: retry from the refreshed mirror
+                } else if (r == -1) {
+                    atomicSub(&A.cnt->free_count, 1);
+                    S.chain_i = -1;
+                } else {
+                    S.chain_i = r;
+                    fetch_row<WT>(A, S, D, cur_buf ^ 1, r);
+                    fetch_rec(A, S, cur_buf ^ 1, r);
+                }
+            }
+            cur_buf ^= 1;
+            __syncthreads();
+            if (S.chain_i < 0) break;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        drain_row(A, S, 0);
+        drain_row(A, S, 1);
+        for (int b = 0; b < 2; ++b)
+            if (S.rec_person[b] >= 0) { mbar_wait(&S.rbar[b], S.rbar_phase[b]); S.rbar_phase[b] ^= 1u; S.rec_person[b] = -1; }
+        if (steps) {
+            atomicAdd(&A.cnt->tail_bids, steps);
+            atomicAdd(&A.cnt->bids, steps);
+            atomicAdd(&A.cnt->scans, scans);
+            atomicAdd(&A.cnt->hits, hits);
+            atomicAdd(&A.cnt->tail_scans, scans);
+        }
+        // every chain must have found its free object before the state is unpacked
+        unsigned ns = 128;
+        while (*reinterpret_cast<volatile int32_t*>(&A.cnt->free_count) != 0) {
+            __nanosleep(ns);
+            ns = ns < 4096 ? ns * 2 : ns;
+        }
+    }
+    grid_barrier(A, grid);
+    for (int64_t t = gtid; t < A.n; t += gsize) {
+        const unsigned long long w = __ldcg(A.word + t);
+        const unsigned long long low = w & A.idmask;
+        A.price[t] = (int64_t)(w >> A.idbits);
+        A.owner[t] = low ? (int32_t)(A.idmask - low) : -1;
+    }
+    grid_barrier(A, grid);
+}
+
 // ---- the persistent solve kernel --------------------------------------------------
 
 template <int WT, bool SP>
@@ -858,6 +1012,12 @@ auction_kernel(AucArgs A) {
             const int cur = r & 1, nxt = cur ^ 1;
             const int32_t count = __ldcg(&A.cnt->list_count[cur]);
             if (count == 0) break;
+            if (count <= A.tail_max && SP && A.async_tail) {
+                const uint64_t t0 = gtimer();
+                tail_async<WT, SP>(A, S, D, eps, count, A.list + (int64_t)cur * A.n_pad, grid);
+                if (blockIdx.x == 0) t_tail += gtimer() - t0;
+                break;
+            }
             if (count <= A.tail_max) {
                 ++tail_epoch;
                 if (blockIdx.x == 0) {
@@ -1108,6 +1268,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     const size_t o_bidj = take(4ull * n_pad);
     const size_t o_bidpk = take(8ull * n_pad);
     const size_t o_cache = take(sizeof(PCache) * (size_t)n_pad);
+    const size_t o_word = take(8ull * n_pad);
     MUX_TRY(ctx->auc.ensure(off));
     char* base = ctx->auc.as<char>();
     AucArgs A;
@@ -1124,9 +1285,10 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.bidj = reinterpret_cast<int32_t*>(base + o_bidj);
     A.bidpk = reinterpret_cast<unsigned long long*>(base + o_bidpk);
     A.cache = reinterpret_cast<PCache*>(base + o_cache);
+    A.word = reinterpret_cast<unsigned long long*>(base + o_word);
     A.SC = n + 1;
     A.theta = theta < 2 ? 2 : theta;
-    A.tail_max = tail_max < 0 ? 0 : (tail_max > kTailMax ? kTailMax : tail_max);
+    A.tail_max = tail_max < 0 ? -1 : (tail_max > kTailMax ? kTailMax : tail_max);
     A.idbits = 1;
     while ((1ll << A.idbits) <= n) ++A.idbits;
     A.idmask = (1ull << A.idbits) - 1ull;
@@ -1162,6 +1324,9 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.round_guard = 200000000ll;
     const char* cgs = getenv("MUX_CG_SYNC");
     A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
+    const char* as = getenv("MUX_ASYNC_TAIL");      // default: on for n >= 2048
+    A.async_tail = (as && *as) ? (*as == '1') : (n >= 2048);
+    if (A.tail_max < 0) A.tail_max = A.async_tail ? 64 : 16;     // auto
     const char* ks = getenv("MUX_K");
     A.keff = (ks && *ks) ? atoi(ks) : kK;
     if (A.keff < 1) A.keff = 1;
@@ -1216,6 +1381,8 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         stats->ms_kernel = hc.ns_total * 1e-6;
         stats->cache_hits = (int64_t)hc.hits;
         stats->launches += launches;
+        if (getenv("MUX_VERBOSE"))
+            fprintf(stderr, "[mux] async-tail rejected bids: %llu\n", hc.async_fail);
         if (getenv("MUX_VERBOSE"))
             fprintf(stderr, "[mux] tail: hits %llu hit-loop cycles/hit %.0f; fetch cycles/scan %.0f\n", hc.tail_hits,
                     hc.cyc_hitloop / (double)(hc.tail_hits + 1), hc.cyc_fetch / (double)(hc.tail_scans + 1));

@@ -321,3 +321,17 @@ def test_golden_pairs_where_optimum_unique(cuda, golden):
         assert [list(p) for p in m.pairs] == case["pairs"]
         checked += 1
     assert checked >= 20
+
+
+@pytest.mark.parametrize("n,m,seed", [(600, 600, 12), (500, 700, 13), (700, 450, 14)])
+def test_async_tail_forced(cuda, monkeypatch, n, m, seed):
+    """The concurrent multi-CTA tail (default for n >= 2048) forced on small
+    problems: optimal totals, valid assignment."""
+    monkeypatch.setenv("MUX_ASYNC_TAIL", "1")
+    _, Q = _pred_Q(n, m, seed, 20)
+    col, total = _gpu_match(Q)
+    want, _ = matching_ref.max_weight_total_int(Q)
+    assert total == want
+    assert matching_ref.assignment_total_int(Q, col) == want
+    used = col[col >= 0]
+    assert len(np.unique(used)) == len(used)
