@@ -1326,7 +1326,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
     const char* as = getenv("MUX_ASYNC_TAIL");      // default: on for n >= 2048
     A.async_tail = (as && *as) ? (*as == '1') : (n >= 2048);
-    if (A.tail_max < 0) A.tail_max = A.async_tail ? 64 : 16;     // auto
+    if (A.tail_max < 0) A.tail_max = 16;     // auto (measured best for both tail modes at 10k)
     const char* ks = getenv("MUX_K");
     A.keff = (ks && *ks) ? atoi(ks) : kK;
     if (A.keff < 1) A.keff = 1;
