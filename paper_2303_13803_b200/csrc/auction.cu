@@ -101,6 +101,7 @@ struct AucArgs {
     int32_t cg_sync;     // 1: cooperative-groups grid.sync, 0: custom barrier
     int32_t keff;        // candidates actually cached (<= kK)
     int32_t async_tail;  // 1: tail chains run concurrently on many CTAs
+    int32_t rot;         // 1 when N != M: per-person rotated tie order (padding entities)
     int64_t eps0;
     int32_t theta;
     int32_t tail_max;
@@ -123,11 +124,41 @@ struct AucArgs {
 
 // ---- keys -------------------------------------------------------------------
 
-__device__ __forceinline__ unsigned long long mkkey(const AucArgs& A, int64_t v, int32_t j) {
-    return ((unsigned long long)(v + A.koff) << A.idbits) | (A.idmask - (unsigned long long)j);
+// Tie order among equal values.  Real (person, object) pairs keep "lowest
+// object index first".  Padding entities are interchangeable, and if they all
+// broke ties the same way every Jacobi round would pile them onto one object,
+// so each person rotates its order over the padding objects (real persons) or
+// over all objects (padding persons) by a per-person offset.  Any fixed order
+// is a valid tie-break; the rotation only spreads the bids.
+__device__ __forceinline__ uint32_t rot_off(int32_t i) { return (uint32_t)i * 2654435761u; }
+__device__ __forceinline__ int32_t tie_rank(const AucArgs& A, int32_t i, int32_t j) {
+    if (!A.rot) return j;
+    if (i >= A.N) {
+        int32_t r = j + (int32_t)(rot_off(i) % (uint32_t)A.n);
+        return r >= A.n ? r - A.n : r;
+    }
+    if (j < A.M) return j;
+    const int32_t D = A.n - A.M;
+    int32_t r = (j - A.M) + (int32_t)(rot_off(i) % (uint32_t)D);
+    return A.M + (r >= D ? r - D : r);
 }
-__device__ __forceinline__ int32_t key_j(const AucArgs& A, unsigned long long k) {
-    return (int32_t)(A.idmask - (k & A.idmask));
+__device__ __forceinline__ int32_t tie_inv(const AucArgs& A, int32_t i, int32_t r) {
+    if (!A.rot) return r;
+    if (i >= A.N) {
+        int32_t j = r - (int32_t)(rot_off(i) % (uint32_t)A.n);
+        return j < 0 ? j + A.n : j;
+    }
+    if (r < A.M) return r;
+    const int32_t D = A.n - A.M;
+    int32_t j = (r - A.M) - (int32_t)(rot_off(i) % (uint32_t)D);
+    return A.M + (j < 0 ? j + D : j);
+}
+
+__device__ __forceinline__ unsigned long long mkkey(const AucArgs& A, int32_t i, int64_t v, int32_t j) {
+    return ((unsigned long long)(v + A.koff) << A.idbits) | (A.idmask - (unsigned long long)tie_rank(A, i, j));
+}
+__device__ __forceinline__ int32_t key_j(const AucArgs& A, int32_t i, unsigned long long k) {
+    return tie_inv(A, i, (int32_t)(A.idmask - (k & A.idmask)));
 }
 __device__ __forceinline__ int64_t key_v(const AucArgs& A, unsigned long long k) {
     return (int64_t)(k >> A.idbits) - A.koff;
@@ -421,7 +452,7 @@ __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, in
         if (j < 0) continue;
         const int64_t a = qk * A.SC;
         const int64_t v = a - pget<SP>(P, j);
-        if (v > v1 || (v == v1 && j < b)) { v2 = v1; v1 = v; b = j; a1 = a; }
+        if (v > v1 || (v == v1 && (b == INT32_MAX || tie_rank(A, i, j) < tie_rank(A, i, b)))) { v2 = v1; v1 = v; b = j; a1 = a; }
         else if (v > v2) v2 = v;
     }
     if (b == INT32_MAX || v1 < thr) return false;
@@ -465,7 +496,7 @@ __device__ __forceinline__ void keys4(const AucArgs& A, const int64_t* P, const 
     wget4<WT>(A, row, i, c, q);
     pget4<SP>(P, c, p);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) k[t] = (c + t < A.n) ? mkkey(A, q[t] * A.SC - p[t], c + t) : kNoKey;
+    for (int t = 0; t < 4; ++t) k[t] = (c + t < A.n) ? mkkey(A, i, q[t] * A.SC - p[t], c + t) : kNoKey;
 }
 
 // Scan a row with the whole CTA: `row` is the staged weight row (or null =
@@ -510,7 +541,10 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
                     if (c + t >= A.n) continue;
                     const int64_t v = q[t] * A.SC - pr[t];
                     gmax[it] = v > gmax[it] ? v : gmax[it];
-                    if (v > bv) { bv = v; bj = c + t; }   // columns ascend: strict > keeps the lowest index
+                    if (v > bv || (A.rot && v == bv && tie_rank(A, i, c + t) < tie_rank(A, i, bj))) {
+                        bv = v;   // columns ascend: without rotation, strict > keeps the lowest index
+                        bj = c + t;
+                    }
                 }
             }
         }
@@ -521,10 +555,10 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
             for (int t = 0; t < 4; ++t) {
                 if (c + t >= A.n) continue;
                 const int64_t v = q[t] * A.SC - pr[t];
-                if (v > bv) { bv = v; bj = c + t; }
+                if (v > bv || (A.rot && v == bv && tie_rank(A, i, c + t) < tie_rank(A, i, bj))) { bv = v; bj = c + t; }
             }
         }
-        unsigned long long mx = bj == INT32_MAX ? kNoKey : mkkey(A, bv, bj);
+        unsigned long long mx = bj == INT32_MAX ? kNoKey : mkkey(A, i, bv, bj);
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {      // half-warp maximum
             const unsigned long long x = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -562,7 +596,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
                 if (c + t >= A.n) continue;
                 const int64_t v = q[t] * A.SC - pr[t];
                 if (v < tau_v) continue;
-                const unsigned long long k = mkkey(A, v, c + t);
+                const unsigned long long k = mkkey(A, i, v, c + t);
                 if (k >= tau) {
                     const int slot = atomicAdd(&S.ncand, 1);
                     if (slot < kCandMax) S.cand[slot] = k;
@@ -577,7 +611,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
                 if (c + t >= A.n) continue;
                 const int64_t v = q[t] * A.SC - pr[t];
                 if (v < tau_v) continue;
-                const unsigned long long k = mkkey(A, v, c + t);
+                const unsigned long long k = mkkey(A, i, v, c + t);
                 if (k >= tau) {
                     const int slot = atomicAdd(&S.ncand, 1);
                     if (slot < kCandMax) S.cand[slot] = k;
@@ -636,7 +670,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
         PCache* rec = A.cache + i;
         if (lane < A.keff) {
             const bool ok = mk != kNoKey;
-            const int32_t j = ok ? key_j(A, mk) : -1;
+            const int32_t j = ok ? key_j(A, i, mk) : -1;
             rec->j[lane] = j;
             int64_t q = 0;
             if (ok && i < A.N && j < A.M) {
@@ -650,7 +684,7 @@ __device__ void cta_scan_bid(const AucArgs& A, Shared& S, const int64_t* P, cons
             const unsigned long long k0 = S.sel[0], k1 = S.sel[1], kt = S.sel[A.keff];
             rec->thr = kt == kNoKey ? kNegInf : key_v(A, kt);
             rec->valid = 1;
-            const int32_t jj = key_j(A, k0);
+            const int32_t jj = key_j(A, i, k0);
             const int64_t v1 = key_v(A, k0);
             const int64_t a1 = v1 + pget<SP>(P, jj);
             S.j1 = jj;
@@ -1324,6 +1358,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.round_guard = 200000000ll;
     const char* cgs = getenv("MUX_CG_SYNC");
     A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
+    A.rot = (N != M) ? 1 : 0;
     const char* as = getenv("MUX_ASYNC_TAIL");      // default: on for n >= 2048
     A.async_tail = (as && *as) ? (*as == '1') : (n >= 2048);
     if (A.tail_max < 0) A.tail_max = 16;     // auto (measured best for both tail modes at 10k)

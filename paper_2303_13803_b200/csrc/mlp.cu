@@ -25,6 +25,8 @@
 
 #include "common.cuh"
 
+
+
 namespace mux {
 
 constexpr int kH = 64;              // hidden width
@@ -34,7 +36,7 @@ constexpr int kSbo = kKg * 128;     // bytes between 8-row core groups (B operan
 constexpr int kSboA = kSbo + 16;    // A operand: +16 B per group rotates banks (conflict-free epilogue stores)
 constexpr int kTile = 128;          // pairs per MMA tile (UMMA M)
 constexpr int kMlpThreads = 128;    // 4 warps = the 4 TMEM lane quadrants
-constexpr int kMlpCtasPerSm = 4;
+template <bool PF> struct MlpCfg { static constexpr int ctas = PF ? 4 : 5; };
 constexpr uint32_t kTmemCols = 64;  // one accumulator reused by layers 2 and 3
 
 struct MlpDev {
@@ -119,8 +121,11 @@ __device__ __forceinline__ uint32_t relu_bf16x2(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-template <int WT>
-__global__ void __launch_bounds__(kMlpThreads, kMlpCtasPerSm)
+// PF = true: the next tile's P/Q rows are prefetched into registers under the
+// current tile's MMAs (4 CTAs/SM); PF = false: each tile batch-loads its own
+// inputs up front, trading the prefetch registers for a fifth CTA per SM.
+template <int WT, bool PF>
+__global__ void __launch_bounds__(kMlpThreads, MlpCfg<PF>::ctas)
 mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
     __shared__ __align__(1024) unsigned char sA[(kTile / 8) * kSboA];  // ~20 KB
     __shared__ __align__(1024) unsigned char sW2[kH * kKp * 2];       // 10 KB
@@ -193,10 +198,11 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
             mma_commit(&mbar);
         }
     };
-    prefetch(blockIdx.x);
+    if (PF) prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int32_t u = (int32_t)(tile / tpr);
         const int32_t v0 = (int32_t)(tile % tpr) * kTile;
+        if (!PF) prefetch(tile);   // batch this tile's loads up front
         if (tid < kH / 4) reinterpret_cast<float4*>(sP)[tid] = pf;
         __syncthreads();
         // ---- h1 = relu(P[u] + Q[v]) -> bf16 into the UMMA layout.  A thread's
@@ -221,7 +227,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         __syncthreads();
         // ---- layer 2 (bias in the ones column) on the tensor cores
         issue_layer(0, w2_addr);
-        prefetch(tile + gridDim.x);           // next tile's inputs load under the MMAs
+        if (PF) prefetch(tile + gridDim.x);   // next tile's inputs load under the MMAs
         bar_wait(&mbar, phase);
         phase ^= 1;
         tc_fence_after();
@@ -380,10 +386,17 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
     p.n = (int32_t)n; p.m = (int32_t)m;
     const int64_t tiles = n * ((m + kTile - 1) / kTile);
     if (tiles > 0) {
-        const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * kMlpCtasPerSm);
+        const char* pv = getenv("MUX_MLP_PREFETCH");
+        const bool pf = pv && *pv == '1';
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * (pf ? MlpCfg<true>::ctas : MlpCfg<false>::ctas));
         const double qscale = ldexp(1.0, qbits);
-        if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
-        else mlp_pairs_kernel<MUX_W_I32><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+        if (pf) {
+            if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32, true><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+            else mlp_pairs_kernel<MUX_W_I32, true><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+        } else {
+            if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32, false><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+            else mlp_pairs_kernel<MUX_W_I32, false><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+        }
         ++*launches;
     }
     MUX_CUDA_TRY(cudaGetLastError());
