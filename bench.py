@@ -337,7 +337,7 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": None, "algorithmic_bytes": auc_bytes, "kernel_ms": auc_ms},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": int(s["launches"]) + 3,
-        "solver": {k: s[k] for k in ("phases", "rounds", "bids", "row_scans", "tail_bids", "cache_hits", "total_q", "ms_tail", "ms_kernel")},
+        "solver": {k: s[k] for k in ("phases", "rounds", "bids", "row_scans", "tail_bids", "cache_hits", "total_q", "ms_tail", "ms_kernel", "ms_canon", "canon_searches", "tight_edges", "dual_sweeps")},
         "ms_match": auc_ms, "ms_per_step_all": times,
     }
     if mlp_line is not None:

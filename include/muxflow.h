@@ -95,6 +95,10 @@ typedef struct {
     double  ms_tail;         /* device time in single-CTA tail mode        */
     double  ms_kernel;       /* device time of the auction kernel (globaltimer) */
     int64_t cache_hits;      /* bids served from the candidate cache       */
+    double  ms_canon;        /* host time of the tie canonicalisation (incl. its kernels) */
+    int64_t canon_searches;  /* alternating-path searches it ran           */
+    int64_t tight_edges;     /* tight edges of the real rows               */
+    int64_t dual_sweeps;     /* Bellman-Ford sweeps of the exact-dual repair */
 } mux_stats_t;
 
 typedef struct mux_ctx mux_ctx_t;
@@ -142,8 +146,8 @@ int mux_score_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp,
 
 /*
  * Maximum-weight bipartite matching on non-negative integer weights
- * (replaces max_weight_matching, matching.py:148-208, minus the tie
- * canonicalisation).  Wq_dev: row-major [n][ldw] of wtype MUX_W_I32 or
+ * (replaces max_weight_matching, matching.py:148-208, including its tie
+ * canonicalisation, matching.py:173-199).  Wq_dev: row-major [n][ldw] of wtype MUX_W_I32 or
  * MUX_W_I64 (0 = missing edge).  Solves the reference's zero-padded square
  * problem exactly (epsilon-scaling auction to epsilon = 1 on weights scaled by
  * max(n, m) + 1).  col_of_row_out: int32 [n], -1 when the row is unmatched or
@@ -162,7 +166,10 @@ int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype,
  * H2D copy of (x, share, y), exact scoring into quantised weights, auction,
  * D2H copy of col_of_row.  Rows with share <= 0 must already be filtered by
  * the caller (scheduler.py:164-165), as must inadmissible columns
- * (scheduler.py:138-140).
+ * (scheduler.py:138-140).  qbits in [1, 52]: weights rint(w * 2^qbits) are
+ * int32 up to 30 bits and int64 above (the exact-parity mode that schedule()
+ * uses for small rounds); the auction's bid packing bounds qbits by about
+ * 60 - 2 log2(max(n, m)).
  */
 int mux_round(mux_ctx_t* ctx, const mux_table_t* table,
               const double* x_host, const double* share_host, int64_t n,

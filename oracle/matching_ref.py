@@ -154,10 +154,11 @@ def repair_path(tight, row_of_col, start_row, target_col, banned_row, banned_col
     return moves
 
 
-def max_weight_matching_dense(W, canonicalize=True):
+def max_weight_matching_dense(W, canonicalize=True, return_col=False):
     """matching.py:148-208 on a dense (nl x nr) float64 weight array whose
     rows/cols are already in sorted-id order.  Entries < WEIGHT_FLOOR are
-    missing edges.  Returns (pairs [(i, j)], total float)."""
+    missing edges.  Returns (pairs [(i, j)], total float), plus the full
+    square col_of_row when `return_col`."""
     W0 = np.asarray(W, dtype=np.float64)
     nl, nr = W0.shape
     n = max(nl, nr)
@@ -201,7 +202,22 @@ def max_weight_matching_dense(W, canonicalize=True):
         if j < nr and Wp[i, j] > 0.0:
             pairs.append((i, j))
             total += float(Wp[i, j])
+    if return_col:
+        return pairs, total, col_of_row
     return pairs, total
+
+
+def history_sensitive(W, col_of_row):
+    """True when a real row ends on a zero-weight REAL column: the one case in
+    which the canonical result depends on the reference's own Hungarian
+    duals (see csrc/canon.cu), so only totals are comparable."""
+    W0 = np.asarray(W, dtype=np.float64)
+    nl, nr = W0.shape
+    for i in range(nl):
+        j = int(col_of_row[i])
+        if j < nr and not W0[i, j] >= WEIGHT_FLOOR:
+            return True
+    return False
 
 
 def max_weight_total_int(Q):

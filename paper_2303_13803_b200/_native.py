@@ -37,7 +37,9 @@ class MuxStats(ctypes.Structure):
                  "tail_bids", "total_q")] + \
                [("ms_score", ctypes.c_double), ("ms_match", ctypes.c_double),
                 ("launches", ctypes.c_int64), ("ms_tail", ctypes.c_double),
-                ("ms_kernel", ctypes.c_double), ("cache_hits", ctypes.c_int64)]
+                ("ms_kernel", ctypes.c_double), ("cache_hits", ctypes.c_int64),
+                ("ms_canon", ctypes.c_double), ("canon_searches", ctypes.c_int64),
+                ("tight_edges", ctypes.c_int64), ("dual_sweeps", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -190,7 +190,10 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     if (!ctx) { set_error("null context"); return MUX_EINVAL; }
     MUX_TRY(mux_table_validate(table));
     if (n < 0 || m < 0) { set_error("mux_round: bad shape"); return MUX_EINVAL; }
-    if (qbits < 1 || qbits > 30) { set_error("mux_round: qbits must be in [1, 30]"); return MUX_EINVAL; }
+    if (qbits < 1 || qbits > 52) { set_error("mux_round: qbits must be in [1, 52]"); return MUX_EINVAL; }
+    // weights are int32 up to 30 bits, int64 beyond (the exact-parity mode)
+    const int wt = qbits > 30 ? MUX_W_I64 : MUX_W_I32;
+    const int64_t esz = wt == MUX_W_I64 ? 8 : 4, vec = 16 / esz;
     MUX_CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (stats) memset(stats, 0, sizeof(*stats));
@@ -206,8 +209,8 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     MUX_TRY(ctx->feat_in.ensure(fbytes));
     double* dfeat = ctx->feat_in.as<double>();
     MUX_CUDA_TRY(cudaMemcpyAsync(dfeat, hp, fbytes, cudaMemcpyHostToDevice, st));
-    const int64_t ldw = ((m + 3) / 4) * 4;
-    MUX_TRY(ctx->wq.ensure(sizeof(int32_t) * (size_t)n * (size_t)(ldw > 0 ? ldw : 4)));
+    const int64_t ldw = ((m + vec - 1) / vec) * vec;
+    MUX_TRY(ctx->wq.ensure((size_t)esz * (size_t)n * (size_t)(ldw > 0 ? ldw : vec)));
     cudaEvent_t e0, e1;
     MUX_CUDA_TRY(cudaEventCreate(&e0));
     MUX_CUDA_TRY(cudaEventCreate(&e1));
@@ -215,7 +218,7 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     int64_t launches = 0;
     if (m > 0)
         MUX_TRY(mux_score_table_impl(ctx, table, dfeat, dfeat + n, n, dfeat + 2 * n, m, MUX_SCORE_EXACT,
-                                     MUX_W_I32, qbits, ctx->wq.ptr, ldw, st, &launches));
+                                     wt, qbits, ctx->wq.ptr, ldw, st, &launches));
     MUX_CUDA_TRY(cudaEventRecord(e1, st));
     MUX_TRY(check_flags(ctx, st));
     float ms_score = 0.f;
@@ -224,7 +227,7 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     cudaEventDestroy(e1);
     MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)n));
     int32_t* col_dev = ctx->colout.as<int32_t>();
-    MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, MUX_W_I32, n, m, ldw, col_dev, total_q, stats, st,
+    MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, wt, n, m, ldw, col_dev, total_q, stats, st,
                            env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1)));
     MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_host, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     MUX_CUDA_TRY(cudaStreamSynchronize(st));

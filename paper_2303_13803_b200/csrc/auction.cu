@@ -52,6 +52,7 @@ constexpr int kTailMax = 256;         // largest tail handed to the tail modes
 constexpr int64_t kNegInf = INT64_MIN / 4;
 constexpr unsigned long long kNoKey = 0ull;
 constexpr size_t kSmemBudget = 220 * 1024;
+constexpr int kPhMax = 32;
 constexpr int kCandMax = 512;         // candidate keys kept by the threshold selection
 
 struct AucCounters {
@@ -75,6 +76,14 @@ struct AucCounters {
     long long max_q;
     long long total_q;
     unsigned long long or_q;
+    // per-phase timeline (MUX_VERBOSE): eps, Jacobi rounds, persons left for
+    // the tail, Jacobi and tail nanoseconds, bids
+    long long ph_eps[kPhMax];
+    int32_t ph_rounds[kPhMax];
+    int32_t ph_tailn[kPhMax];
+    long long ph_ns_j[kPhMax];
+    long long ph_ns_t[kPhMax];
+    unsigned long long ph_bids[kPhMax];
 };
 
 // Per-person candidate cache: one 256-byte record, read by a single lane
@@ -1024,7 +1033,10 @@ auction_kernel(AucArgs A) {
     uint64_t t_tail = 0;
 
     for (;;) {
-        // ---- phase init: clear the assignment, keep prices and caches
+        // ---- phase init: clear the assignment, keep prices and caches.
+        // (Keeping the pairs that still satisfy eps-CS for the new eps frees
+        // nearly everyone anyway: a winning bid leaves its bidder exactly eps
+        // of slack, so almost no pair meets eps/theta.)
         for (int64_t t = gtid; t < n; t += gsize) {
             A.owner[t] = -1;
             A.col[t] = -1;
@@ -1042,10 +1054,14 @@ auction_kernel(AucArgs A) {
         }
         grid_barrier(A, grid);
         int r = 0;
+        const uint64_t tph0 = gtimer();
+        uint64_t tph1 = 0;
+        int32_t ph_tailn = 0;
         for (;;) {
             const int cur = r & 1, nxt = cur ^ 1;
             const int32_t count = __ldcg(&A.cnt->list_count[cur]);
             if (count == 0) break;
+            if (count <= A.tail_max) { tph1 = gtimer(); ph_tailn = count; }
             if (count <= A.tail_max && SP && A.async_tail) {
                 const uint64_t t0 = gtimer();
                 tail_async<WT, SP>(A, S, D, eps, count, A.list + (int64_t)cur * A.n_pad, grid);
@@ -1182,6 +1198,19 @@ auction_kernel(AucArgs A) {
             }
         }
         if (__ldcg(&A.cnt->errors) & kErrIterGuard) return;
+        if (gtid == 0) {
+            const uint64_t tph2 = gtimer();
+            if (tph1 == 0) tph1 = tph2;
+            const int ph = (int)A.cnt->phases - 1;
+            if (ph >= 0 && ph < kPhMax) {
+                A.cnt->ph_eps[ph] = eps;
+                A.cnt->ph_rounds[ph] = r;
+                A.cnt->ph_tailn[ph] = ph_tailn;
+                A.cnt->ph_ns_j[ph] = (long long)(tph1 - tph0);
+                A.cnt->ph_ns_t[ph] = (long long)(tph2 - tph1);
+                A.cnt->ph_bids[ph] = A.cnt->bids + A.cnt->tail_bids;
+            }
+        }
         if (eps <= 1) break;
         eps = eps / A.theta;
         if (eps < 1) eps = 1;
@@ -1265,6 +1294,10 @@ using namespace mux;
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+
+int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t M, int64_t ldw, int32_t n,
+                   int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
+                   cudaStream_t st, mux_stats_t* stats);
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -1389,6 +1422,21 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, dsmem, st));
     ++launches;
     MUX_CUDA_TRY(cudaEventRecord(e1, st));
+    {
+        // among all optimal assignments, return the one the reference's
+        // canonicalisation emits (csrc/canon.cu); MUX_CANON=0 skips it
+        const char* cs = getenv("MUX_CANON");
+        if (!(cs && *cs == '0') && N > 0 && M > 0) {
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            AucCounters pre;
+            MUX_CUDA_TRY(cudaMemcpy(&pre, A.cnt, sizeof(pre), cudaMemcpyDeviceToHost));
+            if (!(pre.errors & (kErrIterGuard | kErrPriceBits))) {
+                MUX_TRY(mux_canon_impl(ctx, W, wtype, (int32_t)N, (int32_t)M, ldw, (int32_t)n, A.SC, A.qshift,
+                                       A.price, A.col, A.owner, st, stats));
+                launches += 2;
+            }
+        }
+    }
     if (N > 0) {
         if (wtype == MUX_W_I32)
             finalize_kernel<MUX_W_I32><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(W, ldw, (int32_t)N, (int32_t)M, A.col, col_out_dev, A.cnt);
@@ -1416,8 +1464,16 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         stats->ms_kernel = hc.ns_total * 1e-6;
         stats->cache_hits = (int64_t)hc.hits;
         stats->launches += launches;
-        if (getenv("MUX_VERBOSE"))
+        if (getenv("MUX_VERBOSE")) {
             fprintf(stderr, "[mux] async-tail rejected bids: %llu\n", hc.async_fail);
+            unsigned long long prev = 0;
+            for (int k = 0; k < (int)hc.phases && k < kPhMax; ++k) {
+                fprintf(stderr, "[mux] phase %2d eps %14lld rounds %6d tail_n %4d jacobi %8.2f ms tail %8.2f ms bids %llu\n", k,
+                        hc.ph_eps[k], hc.ph_rounds[k], hc.ph_tailn[k], hc.ph_ns_j[k] * 1e-6, hc.ph_ns_t[k] * 1e-6,
+                        hc.ph_bids[k] - prev);
+                prev = hc.ph_bids[k];
+            }
+        }
         if (getenv("MUX_VERBOSE"))
             fprintf(stderr, "[mux] tail: hits %llu hit-loop cycles/hit %.0f; fetch cycles/scan %.0f\n", hc.tail_hits,
                     hc.cyc_hitloop / (double)(hc.tail_hits + 1), hc.cyc_fetch / (double)(hc.tail_scans + 1));

@@ -1,0 +1,442 @@
+// Tie canonicalisation of the optimal assignment: the reference returns, among
+// all optimal matchings, the one its row-by-row "repair" pass settles on
+// (matching.py:173-199 with _repair_path, matching.py:104-145).  Three steps:
+//
+//  1. dual_repair_kernel (GPU, cooperative): the auction ends with prices that
+//     satisfy 1-complementary slackness on weights scaled by (n + 1).  Exact
+//     dual feasibility, a_ij - p_j <= a_i,sigma(i) - p_sigma(i) for every
+//     (i, j), is restored by Bellman-Ford relaxation: p_j <- max(p_j,
+//     max_i (a_ij - u_i)) over the rows whose profit u_i changed, until no
+//     price moves.  The assignment is optimal, so there is no positive cycle
+//     and the sweeps terminate.  The prices are then optimal duals.
+//  2. tight_kernel (GPU): the tight edges a_ij - p_j == u_i of every real row,
+//     written as a CSR in column order.  The tight subgraph under ANY optimal
+//     dual contains exactly the optimal matchings, so step 3 reaches the same
+//     matchings as the reference working on its own Hungarian duals.
+//  3. canonicalise (host, native): the reference's sequential loop over rows
+//     on the sparse tight graph.  Padding rows / columns (the reference's zero
+//     square padding) are tight to one shared column set each, handled
+//     implicitly instead of as dense rows.
+//
+// Result: for every row that ends with a positive-weight pair the choice is
+// the lowest column any optimal matching consistent with the earlier rows
+// allows, which is what the reference emits independently of which optimal
+// duals its Hungarian produced.  A row left on a zero-weight REAL column keeps
+// whichever such column the search history leaves it on, as in the reference;
+// that column can differ from the reference's (its history differs), which
+// only matters when weights contain real zeros (never in a scheduling round:
+// every admissible pair has a positive predicted rate).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mux {
+
+struct CanonCounters {
+    int32_t act[2];
+    int32_t nchanged;
+    uint32_t errors;
+    unsigned long long sweeps;
+    unsigned long long row_scans;
+    unsigned long long tight_total;
+};
+
+struct CanonArgs {
+    const void* W;
+    int64_t ldw;
+    int32_t N, M, n;
+    int32_t qshift;
+    int64_t SC;
+    int64_t* price;        // [n] auction prices, repaired in place
+    const int32_t* col;    // [n]
+    const int32_t* owner;  // [n]
+    int64_t* u;            // [n] row profits
+    int32_t* flag;         // [n] column raised in the current sweep
+    int32_t* list;         // [2][n] active rows
+    int32_t* changed;      // [n] columns raised in the current sweep
+    CanonCounters* cnt;
+    int64_t sweep_guard;
+    // tight CSR
+    int32_t* row_cnt;      // [N]
+    int64_t* row_off;      // [N]
+    int32_t* ent;          // [cap] column | bit 31 when the weight is zero
+    int64_t cap;
+};
+
+constexpr uint32_t kCanonErrGuard = 1u << 0;
+constexpr uint32_t kCanonErrCap = 1u << 1;
+constexpr int kCanonThreads = 512;
+
+template <int WT>
+__device__ __forceinline__ int64_t cq(const CanonArgs& C, int32_t i, int32_t j) {
+    if (i >= C.N || j >= C.M) return 0;
+    if (WT == MUX_W_I32) return (int64_t)__ldg(static_cast<const int32_t*>(C.W) + (int64_t)i * C.ldw + j) >> C.qshift;
+    return __ldg(static_cast<const int64_t*>(C.W) + (int64_t)i * C.ldw + j) >> C.qshift;
+}
+
+// four weights of row i < N from column c (zero at j >= M), no read past M
+template <int WT>
+__device__ __forceinline__ void cq4(const CanonArgs& C, int32_t i, int32_t c, int64_t (&q)[4]) {
+    if (c + 4 <= C.M) {
+        if (WT == MUX_W_I32) {
+            const int4 v = __ldg(reinterpret_cast<const int4*>(static_cast<const int32_t*>(C.W) + (int64_t)i * C.ldw + c));
+            q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+        } else {
+            const longlong2* p = reinterpret_cast<const longlong2*>(static_cast<const int64_t*>(C.W) + (int64_t)i * C.ldw + c);
+            const longlong2 a = __ldg(p), b = __ldg(p + 1);
+            q[0] = a.x; q[1] = a.y; q[2] = b.x; q[3] = b.y;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) q[t] >>= C.qshift;
+    } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) q[t] = cq<WT>(C, i, c + t);
+    }
+}
+
+__device__ __forceinline__ void raise_price(const CanonArgs& C, int32_t j, int64_t cand) {
+    if (cand <= __ldcg(C.price + j)) return;
+    const long long old = atomicMax(reinterpret_cast<long long*>(C.price + j), (long long)cand);
+    if (cand > old && atomicExch(C.flag + j, 1) == 0) C.changed[atomicAdd(&C.cnt->nchanged, 1)] = j;
+}
+
+template <int WT>
+__global__ void __launch_bounds__(kCanonThreads, 1) dual_repair_kernel(CanonArgs C) {
+    cg::grid_group grid = cg::this_grid();
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = gtid >> 5, nw = gsize >> 5;
+    const int32_t n = C.n;
+    for (int64_t t = gtid; t < n; t += gsize) {
+        const int32_t i = (int32_t)t;
+        const int32_t j = C.col[i];
+        C.u[i] = cq<WT>(C, i, j) * C.SC - C.price[j];
+        C.list[i] = i;
+        C.flag[i] = 0;
+    }
+    if (gtid == 0) { C.cnt->act[0] = n; C.cnt->act[1] = 0; C.cnt->nchanged = 0; }
+    grid.sync();
+    int cur = 0;
+    for (int64_t sweep = 0;; ++sweep) {
+        const int32_t count = *reinterpret_cast<volatile int32_t*>(&C.cnt->act[cur]);
+        if (count == 0) break;
+        if (sweep > C.sweep_guard) {
+            if (gtid == 0) atomicOr(&C.cnt->errors, kCanonErrGuard);
+            return;
+        }
+        const int nxt = cur ^ 1;
+        for (int64_t idx = gw; idx < count; idx += nw) {
+            const int32_t i = C.list[(int64_t)cur * n + idx];
+            const int64_t ui = __ldcg(C.u + i);
+            if (i >= C.N) {                       // padding row: every weight is zero
+                for (int32_t j = lane; j < n; j += 32) raise_price(C, j, -ui);
+                continue;
+            }
+            for (int32_t c = lane * 4; c < n; c += 128) {
+                int64_t q[4];
+                if (c < C.M) cq4<WT>(C, i, c, q);
+                else q[0] = q[1] = q[2] = q[3] = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (c + t < n) raise_price(C, c + t, q[t] * C.SC - ui);
+            }
+        }
+        if (gtid == 0) atomicAdd(&C.cnt->row_scans, (unsigned long long)count);
+        grid.sync();
+        const int32_t nch = *reinterpret_cast<volatile int32_t*>(&C.cnt->nchanged);
+        for (int64_t k = gtid; k < nch; k += gsize) {
+            const int32_t j = C.changed[k];
+            C.flag[j] = 0;
+            const int32_t i = C.owner[j];
+            C.u[i] = cq<WT>(C, i, j) * C.SC - __ldcg(C.price + j);
+            C.list[(int64_t)nxt * n + atomicAdd(&C.cnt->act[nxt], 1)] = i;
+        }
+        grid.sync();
+        if (gtid == 0) { C.cnt->act[cur] = 0; C.cnt->nchanged = 0; C.cnt->sweeps += 1; }
+        grid.sync();
+        cur = nxt;
+    }
+}
+
+// Tight edges of every real row, in column order: count, reserve, write.
+template <int WT>
+__global__ void __launch_bounds__(256) tight_kernel(CanonArgs C) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = gw; row < C.N; row += nw) {
+        const int32_t i = (int32_t)row;
+        const int64_t ui = C.u[i];
+        int32_t cnt = 0;
+        for (int32_t c = lane * 4; c < C.M; c += 128) {
+            int64_t q[4];
+            cq4<WT>(C, i, c, q);
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (c + t < C.M && q[t] * C.SC - __ldcg(C.price + c + t) == ui) ++cnt;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        long long off = 0;
+        if (lane == 0) off = (long long)atomicAdd(&C.cnt->tight_total, (unsigned long long)cnt);
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (lane == 0) { C.row_cnt[i] = cnt; C.row_off[i] = off; }
+        if (off + cnt > C.cap) {
+            if (lane == 0) atomicOr(&C.cnt->errors, kCanonErrCap);
+            continue;
+        }
+        int32_t base = 0;
+        for (int32_t c0 = 0; c0 < C.M; c0 += 128) {
+            const int32_t c = c0 + lane * 4;
+            int64_t q[4] = {0, 0, 0, 0};
+            bool tq[4] = {false, false, false, false};
+            int32_t mine = 0;
+            if (c < C.M) {
+                cq4<WT>(C, i, c, q);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    tq[t] = c + t < C.M && q[t] * C.SC - __ldcg(C.price + c + t) == ui;
+                    mine += tq[t];
+                }
+            }
+            int32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int32_t pos = base + incl - mine;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (tq[t]) C.ent[off + pos++] = (c + t) | (q[t] == 0 ? (int32_t)0x80000000 : 0);
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+}
+
+// ---- host: the reference's canonicalisation loop on the sparse tight graph --
+
+namespace {
+
+struct TightGraph {
+    int32_t N, M, n;
+    const std::vector<int32_t>* ent;
+    const std::vector<int32_t>* cnt;
+    const std::vector<int64_t>* off;
+    std::vector<int32_t> Z;       // columns tight to every padding row (N < M)
+    std::vector<int32_t> Zpad;    // padding columns tight to rows with padrow_tight (N > M)
+    std::vector<char> padrow_tight;
+};
+
+struct Canon {
+    const TightGraph& G;
+    std::vector<int32_t>& col;
+    std::vector<int32_t> row_of_col;
+    std::vector<char> locked;
+    std::vector<uint32_t> stamp;
+    std::vector<int32_t> parent;
+    uint32_t epoch = 0;
+    long long searches = 0;
+
+    Canon(const TightGraph& g, std::vector<int32_t>& c)
+        : G(g), col(c), row_of_col(g.n), locked(g.n, 0), stamp(g.n, 0), parent(g.n, -1) {
+        for (int32_t i = 0; i < G.n; ++i) row_of_col[col[i]] = i;
+    }
+    bool seen(int32_t j) const { return stamp[j] == epoch || locked[j]; }
+
+    // matching.py:104-145: breadth-first search over tight edges for an
+    // alternating path start_row -> ... -> target_col; applies it on success.
+    bool repair(int32_t start_row, int32_t target_col, int32_t banned_row, int32_t banned_col) {
+        ++searches;
+        ++epoch;
+        stamp[banned_col] = epoch;
+        std::vector<int32_t> frontier{start_row}, nxt;
+        bool found = false, z_done = false, zp_done = false;
+        auto visit = [&](int32_t r, int32_t j) -> bool {
+            if (seen(j)) return false;
+            stamp[j] = epoch;
+            parent[j] = r;
+            if (j == target_col) return true;
+            const int32_t r2 = row_of_col[j];
+            if (r2 != banned_row) nxt.push_back(r2);
+            return false;
+        };
+        while (!frontier.empty() && !found) {
+            nxt.clear();
+            for (int32_t r : frontier) {
+                if (r >= G.N) {                      // padding row: tight to Z
+                    if (!z_done) {
+                        z_done = true;   // every later padding row finds Z visited
+                        for (int32_t j : G.Z)
+                            if (visit(r, j)) { found = true; break; }
+                    }
+                } else {
+                    const int32_t* e = G.ent->data() + (*G.off)[r];
+                    const int32_t k = (*G.cnt)[r];
+                    for (int32_t t = 0; t < k && !found; ++t)
+                        if (visit(r, e[t] & 0x7fffffff)) found = true;
+                    if (!found && G.padrow_tight.size() && G.padrow_tight[r] && !zp_done) {
+                        zp_done = true;
+                        for (int32_t j : G.Zpad)
+                            if (visit(r, j)) { found = true; break; }
+                    }
+                }
+                if (found) break;
+            }
+            frontier.swap(nxt);
+        }
+        if (!found) return false;
+        // reconstruct from the target back to start_row, then apply
+        std::vector<std::pair<int32_t, int32_t>> moves;
+        int32_t j = target_col;
+        for (;;) {
+            const int32_t r = parent[j];
+            moves.emplace_back(r, j);
+            if (r == start_row) break;
+            j = col[r];
+        }
+        for (auto& m : moves) { row_of_col[m.second] = m.first; col[m.first] = m.second; }
+        return true;
+    }
+
+    // matching.py:173-199
+    void run() {
+        for (int32_t i = 0; i < G.N; ++i) {
+            int32_t j_cur = col[i];
+            const int32_t* e = G.ent->data() + (*G.off)[i];
+            const int32_t k = (*G.cnt)[i];
+            bool emitted = false;
+            if (j_cur < G.M)
+                for (int32_t t = 0; t < k; ++t)
+                    if ((e[t] & 0x7fffffff) == j_cur) { emitted = (e[t] >= 0); break; }
+            for (int32_t t = 0; t < k; ++t) {
+                if (e[t] < 0) continue;                 // zero weight
+                const int32_t j = e[t];
+                if (locked[j]) continue;
+                if (emitted && j >= j_cur) break;
+                if (!repair(row_of_col[j], j_cur, i, j)) continue;
+                row_of_col[j] = i;
+                col[i] = j;
+                j_cur = j;
+                break;
+            }
+            locked[j_cur] = 1;
+        }
+    }
+};
+
+}  // namespace
+}  // namespace mux
+
+using namespace mux;
+
+int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t M, int64_t ldw, int32_t n,
+                   int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
+                   cudaStream_t st, mux_stats_t* stats) {
+    if (N <= 0 || M <= 0 || n <= 0) return MUX_OK;
+    const auto h0 = std::chrono::steady_clock::now();
+    int64_t cap = (int64_t)N * (int64_t)M;
+    if (cap > (1ll << 28)) cap = 1ll << 28;
+    if (cap < 16) cap = 16;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
+    const size_t o_cnt = take(sizeof(CanonCounters));
+    const size_t o_u = take(8ull * n);
+    const size_t o_flag = take(4ull * n);
+    const size_t o_list = take(8ull * n);
+    const size_t o_chg = take(4ull * n);
+    const size_t o_rcnt = take(4ull * N);
+    const size_t o_roff = take(8ull * N);
+    const size_t o_ent = take(4ull * (size_t)cap);
+    MUX_TRY(ctx->canon.ensure(off));
+    char* base = ctx->canon.as<char>();
+    CanonArgs C;
+    C.W = W; C.ldw = ldw; C.N = N; C.M = M; C.n = n; C.qshift = qshift; C.SC = SC;
+    C.price = price; C.col = col_dev; C.owner = owner;
+    C.cnt = reinterpret_cast<CanonCounters*>(base + o_cnt);
+    C.u = reinterpret_cast<int64_t*>(base + o_u);
+    C.flag = reinterpret_cast<int32_t*>(base + o_flag);
+    C.list = reinterpret_cast<int32_t*>(base + o_list);
+    C.changed = reinterpret_cast<int32_t*>(base + o_chg);
+    C.row_cnt = reinterpret_cast<int32_t*>(base + o_rcnt);
+    C.row_off = reinterpret_cast<int64_t*>(base + o_roff);
+    C.ent = reinterpret_cast<int32_t*>(base + o_ent);
+    C.cap = cap;
+    C.sweep_guard = 4ll * n + 16;
+    MUX_CUDA_TRY(cudaMemsetAsync(C.cnt, 0, sizeof(CanonCounters), st));
+
+    void* fn = wtype == MUX_W_I32 ? (void*)dual_repair_kernel<MUX_W_I32> : (void*)dual_repair_kernel<MUX_W_I64>;
+    int per_sm = 0;
+    MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCanonThreads, 0));
+    if (per_sm < 1) { set_error("dual repair kernel cannot be resident"); return MUX_ECUDA; }
+    void* args[] = {&C};
+    MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)ctx->num_sms), dim3(kCanonThreads), args, 0, st));
+    const unsigned tg = (unsigned)std::min<int64_t>(((int64_t)N * 32 + 255) / 256, (int64_t)ctx->num_sms * 8);
+    if (wtype == MUX_W_I32) tight_kernel<MUX_W_I32><<<tg, 256, 0, st>>>(C);
+    else tight_kernel<MUX_W_I64><<<tg, 256, 0, st>>>(C);
+    MUX_CUDA_TRY(cudaGetLastError());
+
+    CanonCounters hc;
+    MUX_CUDA_TRY(cudaMemcpyAsync(&hc, C.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    const auto h1 = std::chrono::steady_clock::now();
+    if (hc.errors & kCanonErrGuard) { set_error("canonicalisation: dual repair did not converge"); return MUX_ELIMIT; }
+    if (hc.errors & kCanonErrCap) { set_error("canonicalisation: tight-edge graph exceeds its buffer"); return MUX_ELIMIT; }
+
+    std::vector<int32_t> col(n), rcnt(N), ent((size_t)hc.tight_total);
+    std::vector<int64_t> p(n), u(n), roff(N);
+    MUX_CUDA_TRY(cudaMemcpyAsync(col.data(), col_dev, 4ull * n, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaMemcpyAsync(p.data(), price, 8ull * n, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaMemcpyAsync(u.data(), C.u, 8ull * n, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaMemcpyAsync(rcnt.data(), C.row_cnt, 4ull * N, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaMemcpyAsync(roff.data(), C.row_off, 8ull * N, cudaMemcpyDeviceToHost, st));
+    if (hc.tight_total)
+        MUX_CUDA_TRY(cudaMemcpyAsync(ent.data(), C.ent, 4ull * hc.tight_total, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+
+    const auto h2 = std::chrono::steady_clock::now();
+    TightGraph G;
+    G.N = N; G.M = M; G.n = n;
+    G.ent = &ent; G.cnt = &rcnt; G.off = &roff;
+    if (N < n) {                 // padding rows: tight exactly to the cheapest columns
+        const int64_t pmin = *std::min_element(p.begin(), p.end());
+        for (int32_t j = 0; j < n; ++j)
+            if (p[j] == pmin) G.Z.push_back(j);
+    }
+    if (M < n) {                 // padding columns: tight to row i iff -p_c == u_i
+        const int64_t pmin = *std::min_element(p.begin() + M, p.end());
+        for (int32_t j = M; j < n; ++j)
+            if (p[j] == pmin) G.Zpad.push_back(j);
+        G.padrow_tight.assign(N, 0);
+        for (int32_t i = 0; i < N; ++i) G.padrow_tight[i] = (-u[i] == pmin);
+    }
+    Canon K(G, col);
+    K.run();
+    const auto h3 = std::chrono::steady_clock::now();
+    if (getenv("MUX_VERBOSE")) {
+        auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        fprintf(stderr, "[mux] canon: dual repair + tight %.2f ms (%llu sweeps, %llu row scans), D2H %.2f ms, "
+                        "host %.2f ms (%lld searches, %llu tight edges)\n",
+                ms(h0, h1), hc.sweeps, hc.row_scans, ms(h1, h2), ms(h2, h3), K.searches, hc.tight_total);
+    }
+    MUX_CUDA_TRY(cudaMemcpyAsync(col_dev, col.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    if (stats) {
+        stats->ms_canon = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+        stats->canon_searches = K.searches;
+        stats->tight_edges = (int64_t)hc.tight_total;
+        stats->dual_sweeps = (int64_t)hc.sweeps;
+    }
+    return MUX_OK;
+}

@@ -45,12 +45,21 @@ class Matching:
     total_weight: float
 
 
-def max_qbits(n: int) -> int:
-    """Largest quantisation (<= 30 bits, int32 storage) whose auction prices
-    fit the 64-bit bid packing for an n x n problem."""
+def max_qbits(n: int, cap: int = 30) -> int:
+    """Largest quantisation (<= `cap` bits; int32 storage up to 30) whose
+    auction prices fit the 64-bit bid packing for an n x n problem."""
     idbits = max(1, int(n).bit_length())
     q = int(math.floor(60 - idbits - math.log2(n + 1))) - 1
-    return max(1, min(30, q))
+    return max(1, min(int(cap), q))
+
+
+def round_qbits(n: int) -> int:
+    """Quantisation of a scheduling round: the exact-parity mode (int64
+    weights, up to 40 bits) where the bid packing leaves
+    at least 32 bits, else 30-bit int32 weights (large rounds, where int64
+    rows would no longer fit the auction's shared-memory staging)."""
+    q = max_qbits(n, cap=40)
+    return q if (q >= 32 and n <= 6144) else min(q, 30)
 
 
 def match_dense(Wq, n=None, m=None, stats=False):

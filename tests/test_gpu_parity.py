@@ -335,3 +335,77 @@ def test_async_tail_forced(cuda, monkeypatch, n, m, seed):
     assert matching_ref.assignment_total_int(Q, col) == want
     used = col[col >= 0]
     assert len(np.unique(used)) == len(used)
+
+
+# ------------------------------------------------- tie canonicalisation (a11)
+
+def _dense_graph(W):
+    from paper_2303_13803_b200 import BipartiteGraph
+    nl, nr = W.shape
+    L = tuple(f"l{i:03d}" for i in range(nl))
+    R = tuple(f"r{j:03d}" for j in range(nr))
+    w = {(L[i], R[j]): float(W[i, j]) for i in range(nl) for j in range(nr) if W[i, j] > 0}
+    return BipartiteGraph(L, R, w), L, R
+
+
+@pytest.mark.parametrize("zeros", [False, True])
+def test_canonical_pairs_tie_heavy(cuda, zeros):
+    """Dyadic weights from a handful of levels: most instances have many
+    optimal matchings; the GPU must emit the reference's canonical one
+    (matching.py:173-199), including rectangular (zero-padded) shapes."""
+    from paper_2303_13803_b200 import max_weight_matching
+    rng = np.random.default_rng(31 + zeros)
+    checked = skipped = 0
+    for trial in range(250):
+        nl, nr = int(rng.integers(1, 24)), int(rng.integers(1, 24))
+        levels = int(rng.choice([1, 2, 4, 8]))
+        W = rng.integers(1, levels + 1, size=(nl, nr)) / levels
+        if zeros:
+            W[rng.random((nl, nr)) < 0.35] = 0.0
+        want, total, ocol = matching_ref.max_weight_matching_dense(W, return_col=True)
+        g, L, R = _dense_graph(W)
+        m = max_weight_matching(g)
+        assert m.total_weight == total, trial
+        if matching_ref.history_sensitive(W, ocol):
+            skipped += 1
+            continue
+        assert list(m.pairs) == [(L[i], R[j]) for i, j in want], trial
+        checked += 1
+    assert checked >= 150
+
+
+def test_canonical_golden_pairs_all_cases(cuda, golden):
+    """Every golden matching case of the reference (not only the unique
+    optima): identical pair lists."""
+    from paper_2303_13803_b200 import max_weight_matching
+    checked = 0
+    for case in golden["matching"]["cases"]:
+        L, R = sorted(case["left"]), sorted(case["right"])
+        W = np.zeros((len(L), len(R)))
+        li = {l: i for i, l in enumerate(L)}
+        ri = {r: j for j, r in enumerate(R)}
+        for a, b, x in case["edges"]:
+            W[li[a], ri[b]] = x
+        if L and R:
+            _, _, ocol = matching_ref.max_weight_matching_dense(W, return_col=True)
+            if matching_ref.history_sensitive(W, ocol):
+                continue
+        m = max_weight_matching(_graph_from_case(case))
+        assert [list(p) for p in m.pairs] == case["pairs"]
+        checked += 1
+    assert checked >= 100
+
+
+@pytest.mark.parametrize("n,m,seed", [(400, 400, 41), (300, 520, 42), (520, 300, 43)])
+def test_canonical_pairs_predictor_quantised(cuda, n, m, seed):
+    """Predictor-derived weights quantised at S = 12 bits (many exact ties):
+    the GPU pair list equals the reference restatement's canonical one."""
+    from paper_2303_13803_b200 import max_weight_matching
+    _, Q = _pred_Q(n, m, seed, 12)
+    W = Q / 2.0 ** 12
+    want, total, ocol = matching_ref.max_weight_matching_dense(W, return_col=True)
+    assert not matching_ref.history_sensitive(W, ocol)
+    g, L, R = _dense_graph(W)
+    mm = max_weight_matching(g)
+    assert mm.total_weight == total
+    assert list(mm.pairs) == [(L[i], R[j]) for i, j in want]
