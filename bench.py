@@ -1,12 +1,15 @@
 """Benchmark: one MuxFlow scheduling round (predict + optimal match) at 10k x 10k.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--n 10000] [--m 10000] [--qbits 20]
+                    [--n 10000] [--m 10000] [--qbits 30]
 
 A step is one full round over one synthetic cluster snapshot:
 exact float64 scoring of every (online, offline) pair into int32 weights
-rint(w * 2^20) (csrc/score.cu), then the epsilon-scaling auction
-(csrc/auction.cu) to the exact optimum.  `value` is ms per round with the
+rint(w * 2^30) (csrc/score.cu; 30 bits is the finest int32 quantisation and the
+closest to the reference's float64 weights -- SURVEY's S = 20 is available
+with --qbits 20 and has ~14x more tight (tied) edges), then the
+epsilon-scaling auction (csrc/auction.cu) to the exact optimum and the tie
+canonicalisation (csrc/canon.cu).  `value` is ms per round with the
 feature arrays already resident in HBM (device-timed with CUDA events on the
 launching stream); `e2e` is the same round through the C-ABI `mux_round` with
 HOST feature arrays (H2D of features and D2H of col_of_row inside the timed
@@ -44,7 +47,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--n", type=int, default=10000)
     p.add_argument("--m", type=int, default=10000)
-    p.add_argument("--qbits", type=int, default=20)
+    p.add_argument("--qbits", type=int, default=30)
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")

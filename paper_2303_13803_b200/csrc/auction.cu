@@ -84,6 +84,9 @@ struct AucCounters {
     long long ph_ns_j[kPhMax];
     long long ph_ns_t[kPhMax];
     unsigned long long ph_bids[kPhMax];
+    unsigned long long ph_maxchain[kPhMax];   // async chains: longest chain (bids)
+    unsigned long long ph_longchains[kPhMax]; // async chains: chains of more than 256 bids
+    unsigned long long ph_chains[kPhMax];
 };
 
 // Per-person candidate cache: one 256-byte record, read by a single lane
@@ -111,6 +114,10 @@ struct AucArgs {
     int32_t keff;        // candidates actually cached (<= kK)
     int32_t async_tail;  // 1: tail chains run concurrently on many CTAs
     int32_t rot;         // 1 when N != M: per-person rotated tie order (padding entities)
+    int32_t async_phases;  // leading phases run entirely as concurrent chains (no Jacobi rounds)
+    int32_t fresh;         // async chains: cache bids read current prices (not the CTA mirror)
+    int32_t restage;       // async chains: re-stage the price mirror before every row scan
+    int32_t order;         // async chains: queue persons by their previous object's price
     int64_t eps0;
     int32_t theta;
     int32_t tail_max;
@@ -436,7 +443,8 @@ __device__ __forceinline__ int64_t bid_from(int64_t a1, int64_t v1, int64_t seco
 // hit; ties on value go to the lower object index, like a full scan.
 template <bool SP>
 __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, int32_t i, int64_t eps,
-                                          int32_t& j1, int64_t& bid, const PCache* srec = nullptr) {
+                                          int32_t& j1, int64_t& bid, const PCache* srec = nullptr,
+                                          int64_t* fresh_mirror = nullptr) {
     const longlong2* rec = reinterpret_cast<const longlong2*>(A.cache + i);
     longlong2 w[13];     // j[0..16) | q[0..16) | thr, valid
     if (srec) {          // prefetched copy in shared memory
@@ -460,7 +468,14 @@ __device__ __forceinline__ bool cache_bid(const AucArgs& A, const int64_t* P, in
         const int64_t qk = (k & 1) ? w[4 + (k >> 1)].y : w[4 + (k >> 1)].x;
         if (j < 0) continue;
         const int64_t a = qk * A.SC;
-        const int64_t v = a - pget<SP>(P, j);
+        int64_t pj;
+        if (fresh_mirror) {      // async tail: current price from the packed word, mirror refreshed
+            pj = (int64_t)(__ldcg(A.word + j) >> A.idbits);
+            fresh_mirror[j] = pj;
+        } else {
+            pj = pget<SP>(P, j);
+        }
+        const int64_t v = a - pj;
         if (v > v1 || (v == v1 && (b == INT32_MAX || tie_rank(A, i, j) < tie_rank(A, i, b)))) { v2 = v1; v1 = v; b = j; a1 = a; }
         else if (v > v2) v2 = v;
     }
@@ -892,7 +907,7 @@ __device__ __forceinline__ void stage_word_prices(const AucArgs& A, int64_t* sp)
 
 template <int WT, bool SP>
 __device__ void tail_async(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int32_t count, const int32_t* src,
-                           cg::grid_group& grid) {
+                           cg::grid_group& grid, int ph) {
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsize = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = gtid; t < A.n_pad; t += gsize)
@@ -914,6 +929,7 @@ __device__ void tail_async(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int
         if (S.chain_i < 0) break;
         stage_word_prices(A, D.price);
         __syncthreads();
+        const unsigned long long steps0 = steps;
         for (;;) {
             if (threadIdx.x == 0) {
                 int32_t cur = S.chain_i;
@@ -923,7 +939,7 @@ __device__ void tail_async(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int
                     int32_t j1 = 0;
                     int64_t bid = 0;
                     const PCache* srec = claim_rec(S, cur_buf, cur);
-                    if (!cache_bid<SP>(A, P, cur, eps, j1, bid, srec)) { need = cur; break; }
+                    if (!cache_bid<SP>(A, P, cur, eps, j1, bid, srec, (SP && A.fresh) ? D.price : nullptr)) { need = cur; break; }
                     const int32_t r = async_commit<SP>(A, D, cur, j1, bid);
                     ++steps;
                     if (r == -2) { ++fails; continue; }
@@ -938,6 +954,10 @@ __device__ void tail_async(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int
             __syncthreads();
             const int32_t i = S.scan_i;
             if (i < 0) break;                      // chain finished
+            if (A.restage) {
+                stage_word_prices(A, D.price);
+                __syncthreads();
+            }
             const void* row = wait_row<WT>(A, S, D, cur_buf, i);
             cta_scan_bid<WT, SP>(A, S, P, row, i, eps);
             if (threadIdx.x == 0) {
@@ -960,6 +980,12 @@ __device__ void tail_async(const AucArgs& A, Shared& S, Dyn& D, int64_t eps, int
             cur_buf ^= 1;
             __syncthreads();
             if (S.chain_i < 0) break;
+        }
+        if (threadIdx.x == 0 && ph < kPhMax) {
+            const unsigned long long len = steps - steps0;
+            atomicMax(&A.cnt->ph_maxchain[ph], len);
+            atomicAdd(&A.cnt->ph_chains[ph], 1ull);
+            if (len > 256) atomicAdd(&A.cnt->ph_longchains[ph], 1ull);
         }
         __syncthreads();
     }
@@ -1031,16 +1057,36 @@ auction_kernel(AucArgs A) {
     uint64_t t_a1 = 0, t_a2 = 0, t_b = 0;
     const uint64_t t_start = gtimer();
     uint64_t t_tail = 0;
+    int phase_no = 0;
 
     for (;;) {
         // ---- phase init: clear the assignment, keep prices and caches.
         // (Keeping the pairs that still satisfy eps-CS for the new eps frees
         // nearly everyone anyway: a winning bid leaves its bidder exactly eps
         // of slack, so almost no pair meets eps/theta.)
+        const bool chains = SP && A.async_tail && phase_no < A.async_phases;
+        if (chains && phase_no > 0 && A.order) {
+            // queue the persons by the price of the object they held in the
+            // previous phase, most expensive first: each one then tends to find
+            // its object free and the displacement chains stay short
+            stage_prices(A, D.price, nullptr);
+            __syncthreads();
+            for (int64_t t = gtid; t < n; t += gsize) {
+                const int32_t j = (int32_t)t;
+                const int64_t pj = lds_ll(smem_u32(D.price + j));
+                int32_t rank = 0;
+                for (int32_t k = 0; k < n; ++k) {
+                    const int64_t pk = lds_ll(smem_u32(D.price + k));
+                    rank += (pk > pj) || (pk == pj && k < j);
+                }
+                A.list[rank] = A.owner[j];
+            }
+            grid_barrier(A, grid);
+        }
         for (int64_t t = gtid; t < n; t += gsize) {
             A.owner[t] = -1;
             A.col[t] = -1;
-            A.list[t] = (int32_t)t;          // list[0]
+            if (!(chains && phase_no > 0 && A.order)) A.list[t] = (int32_t)t;          // list[0]
             A.bidw[t] = 0ull;
             A.bidw[A.n_pad + t] = 0ull;
         }
@@ -1062,9 +1108,9 @@ auction_kernel(AucArgs A) {
             const int32_t count = __ldcg(&A.cnt->list_count[cur]);
             if (count == 0) break;
             if (count <= A.tail_max) { tph1 = gtimer(); ph_tailn = count; }
-            if (count <= A.tail_max && SP && A.async_tail) {
+            if (SP && A.async_tail && (count <= A.tail_max || (r == 0 && phase_no < A.async_phases))) {
                 const uint64_t t0 = gtimer();
-                tail_async<WT, SP>(A, S, D, eps, count, A.list + (int64_t)cur * A.n_pad, grid);
+                tail_async<WT, SP>(A, S, D, eps, count, A.list + (int64_t)cur * A.n_pad, grid, phase_no);
                 if (blockIdx.x == 0) t_tail += gtimer() - t0;
                 break;
             }
@@ -1212,6 +1258,7 @@ auction_kernel(AucArgs A) {
             }
         }
         if (eps <= 1) break;
+        ++phase_no;
         eps = eps / A.theta;
         if (eps < 1) eps = 1;
     }
@@ -1298,6 +1345,11 @@ using namespace mux;
 int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t M, int64_t ldw, int32_t n,
                    int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
                    cudaStream_t st, mux_stats_t* stats);
+
+static int env_flag(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -1392,9 +1444,17 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     const char* cgs = getenv("MUX_CG_SYNC");
     A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
     A.rot = (N != M) ? 1 : 0;
-    const char* as = getenv("MUX_ASYNC_TAIL");      // default: on for n >= 2048
-    A.async_tail = (as && *as) ? (*as == '1') : (n >= 2048);
-    if (A.tail_max < 0) A.tail_max = 16;     // auto (measured best for both tail modes at 10k)
+    const char* as = getenv("MUX_ASYNC_TAIL");      // default: on for n >= 512
+    A.async_tail = (as && *as) ? (*as == '1') : (n >= 512);
+    if (A.tail_max < 0) A.tail_max = 16;
+    const char* ap = getenv("MUX_ASYNC_PHASES");
+    // with the concurrent chains on, every phase runs as chains (no Jacobi
+    // rounds): on near-rank-1 weights a Jacobi round settles ~1 person when
+    // everyone bids for the same object (10k: 9,400 rounds in phase 0)
+    A.async_phases = (ap && *ap) ? atoi(ap) : 1 << 20;
+    A.fresh = env_flag("MUX_FRESH", 1);
+    A.restage = env_flag("MUX_RESTAGE", 0);
+    A.order = env_flag("MUX_ORDER", 1);     // auto (measured best for both tail modes at 10k)
     const char* ks = getenv("MUX_K");
     A.keff = (ks && *ks) ? atoi(ks) : kK;
     if (A.keff < 1) A.keff = 1;
@@ -1468,9 +1528,10 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             fprintf(stderr, "[mux] async-tail rejected bids: %llu\n", hc.async_fail);
             unsigned long long prev = 0;
             for (int k = 0; k < (int)hc.phases && k < kPhMax; ++k) {
-                fprintf(stderr, "[mux] phase %2d eps %14lld rounds %6d tail_n %4d jacobi %8.2f ms tail %8.2f ms bids %llu\n", k,
+                fprintf(stderr, "[mux] phase %2d eps %14lld rounds %6d tail_n %4d jacobi %8.2f ms tail %8.2f ms bids %llu"
+                                " chains %llu long %llu max %llu\n", k,
                         hc.ph_eps[k], hc.ph_rounds[k], hc.ph_tailn[k], hc.ph_ns_j[k] * 1e-6, hc.ph_ns_t[k] * 1e-6,
-                        hc.ph_bids[k] - prev);
+                        hc.ph_bids[k] - prev, hc.ph_chains[k], hc.ph_longchains[k], hc.ph_maxchain[k]);
                 prev = hc.ph_bids[k];
             }
         }
