@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmuxflow.so")
-SOURCES = ("api.cu", "score.cu", "auction.cu", "canon.cu", "mlp.cu")
+SOURCES = ("api.cu", "score.cu", "auction.cu", "ssp.cu", "canon.cu", "mlp.cu")
 HEADERS = ("common.cuh",)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
@@ -23,17 +23,45 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+OBJDIR = os.path.join(HERE, "build")
+
+
+def _compile(nvcc, src, obj, force):
+    """One translation unit -> object (skipped when the object is newer than
+    the source and the shared headers)."""
+    deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(HERE, "..", "include", "muxflow.h")]
+    if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
+        return None
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    return subprocess.Popen([nvcc] + flags + ["-c", src, "-o", obj], stdout=subprocess.PIPE,
+                            stderr=subprocess.PIPE, text=True)
+
+
 def build(force=False, verbose=False):
     if not force and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-o", OUT + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs, procs = [], []
+    for f in SOURCES:
+        obj = os.path.join(OBJDIR, f.replace(".cu", ".o"))
+        objs.append(obj)
+        p = _compile(nvcc, os.path.join(CSRC, f), obj, force)
+        if p is not None:
+            procs.append((f, p))
+    for f, p in procs:   # translation units compile in parallel
+        out, err = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError(f"nvcc failed compiling {f}")
+        if verbose:
+            sys.stderr.write(err)
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+           "-o", OUT + ".tmp"] + objs
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libmuxflow.so")
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc failed linking libmuxflow.so")
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

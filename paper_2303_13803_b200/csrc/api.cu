@@ -14,7 +14,7 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
                        cudaStream_t st, int64_t* launches);
 int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
                    int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
-                   int theta, int tail_max);
+                   int theta, int tail_max, const double* rowkey, const double* colkey);
 
 namespace mux {
 static thread_local std::string g_last_error;
@@ -81,7 +81,7 @@ int mux_ctx_destroy(mux_ctx_t* ctx) {
     if (!ctx) return MUX_OK;
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->table, &ctx->rowfeat, &ctx->colfeat, &ctx->flags, &ctx->feat_in, &ctx->wq,
-                      &ctx->colout, &ctx->auc, &ctx->mlp})
+                      &ctx->colout, &ctx->auc, &ctx->ssp, &ctx->canon, &ctx->mlp})
         b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
@@ -176,7 +176,7 @@ int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t 
     }
     if (stats) memset(stats, 0, sizeof(*stats));
     MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1)));
+                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1), nullptr, nullptr));
     if (out_on_host && n > 0) {
         MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));
@@ -227,8 +227,9 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     cudaEventDestroy(e1);
     MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)n));
     int32_t* col_dev = ctx->colout.as<int32_t>();
+    // ordering keys for the multilevel solver: the online / offline SM demand
     MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, wt, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1)));
+                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1), x_host, y_host));
     MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_host, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     if (stats) {

@@ -38,6 +38,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdio>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -1334,6 +1335,14 @@ __global__ void finalize_kernel(const void* W, int64_t ldw, int32_t N, int32_t M
     if ((threadIdx.x & 31) == 0 && q) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->total_q), (unsigned long long)q);
 }
 
+__global__ void finalize_ssp_kernel(const int32_t* W, int64_t ldw, int32_t n, const int32_t* col, int32_t* out) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        const int32_t j = col[i];
+        out[i] = (j >= 0 && j < n && W[(int64_t)i * ldw + j] > 0) ? j : -1;
+    }
+}
+
 }  // namespace mux
 
 using namespace mux;
@@ -1353,9 +1362,18 @@ static int env_flag(const char* name, int dflt) {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const double* rowkey,
+                 const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
+                 int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st);
+
+__global__ void scale_price_kernel(int64_t* p, int32_t n, int64_t sc) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) p[j] *= sc;
+}
+
 int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
                    int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
-                   int theta, int tail_max) {
+                   int theta, int tail_max, const double* rowkey, const double* colkey) {
     if (N < 0 || M < 0 || (N > 0 && ldw < M)) { set_error("mux_match: bad shape"); return MUX_EINVAL; }
     if (wtype != MUX_W_I32 && wtype != MUX_W_I64) { set_error("mux_match: weights must be int32 or int64"); return MUX_EINVAL; }
     const int64_t n = N > M ? N : M;
@@ -1369,6 +1387,39 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     }
     if (total_q) *total_q = 0;
     if (n == 0) return MUX_OK;
+    {
+        // Square int32 problems: multilevel shortest-path solver (csrc/ssp.cu);
+        // MUX_SOLVER=auction selects the epsilon-scaling auction below.
+        const char* sv = getenv("MUX_SOLVER");
+        const bool use_ssp = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && N == M && N >= 2;
+        if (use_ssp) {
+            const int32_t nn = (int32_t)N;
+            const size_t o_p = 0, o_c = (8ull * nn + 255) & ~255ull, o_o = o_c + ((4ull * nn + 255) & ~255ull);
+            MUX_TRY(ctx->auc.ensure(o_o + 4ull * nn + 256));
+            char* base = ctx->auc.as<char>();
+            int64_t* price = reinterpret_cast<int64_t*>(base + o_p);
+            int32_t* colr = reinterpret_cast<int32_t*>(base + o_c);
+            int32_t* owner = reinterpret_cast<int32_t*>(base + o_o);
+            int64_t tq = 0;
+            MUX_TRY(mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, nn, rowkey, colkey, col_out_dev, &tq,
+                                 price, colr, owner, stats, st));
+            const char* cs = getenv("MUX_CANON");
+            if (!(cs && *cs == '0')) {
+                // canonicalisation works in the auction's units: benefits Q * (n + 1)
+                scale_price_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(price, nn, (int64_t)nn + 1);
+                MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, nn, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats));
+                // the canonical assignment has the same (optimal) total
+                finalize_ssp_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
+                    static_cast<const int32_t*>(W), ldw, nn, colr, col_out_dev);
+                MUX_CUDA_TRY(cudaGetLastError());
+                MUX_CUDA_TRY(cudaStreamSynchronize(st));
+                if (stats) stats->launches += 4;
+            }
+            if (total_q) *total_q = tq;
+            if (stats) stats->total_q = tq;
+            return MUX_OK;
+        }
+    }
     const int32_t n_pad = (int32_t)(((n + 3) / 4) * 4 + 4);
     // a staged row covers columns [0, M) rounded up to 16 bytes (<= ldw)
     int64_t row_cols = ((M + 3) / 4) * 4;

@@ -82,6 +82,8 @@ struct mux_ctx {
     mux::DevBuf colout;     // int32 col_of_row on device
     // auction workspace
     mux::DevBuf auc;
+    // multilevel shortest-path solver workspace (csrc/ssp.cu)
+    mux::DevBuf ssp;
     // tie canonicalisation workspace (duals, tight-edge CSR)
     mux::DevBuf canon;
     // MLP plugin parameters + layer-1 partials
