@@ -220,8 +220,9 @@ def run_ours(args, rank, world, local_rank):
     def step():
         nat.check(lib.mux_score_table(ctx, tb, xd.data_ptr(), sd.data_ptr(), n, yd.data_ptr(), m,
                                       nat.MUX_SCORE_EXACT, nat.MUX_W_I32, q, Wq.data_ptr(), ldw, sptr))
-        nat.check(lib.mux_match(ctx, Wq.data_ptr(), nat.MUX_W_I32, n, m, ldw, col.data_ptr(), 0,
-                                nat.ctypes.byref(total), nat.ctypes.byref(st), sptr))
+        # the online / offline SM demands order rows and columns for the solver's warm start
+        nat.check(lib.mux_match_keyed(ctx, Wq.data_ptr(), nat.MUX_W_I32, n, m, ldw, xd.data_ptr(), yd.data_ptr(),
+                                      col.data_ptr(), 0, nat.ctypes.byref(total), nat.ctypes.byref(st), sptr))
         return st.as_dict(), int(total.value)
 
     for _ in range(args.warmup):

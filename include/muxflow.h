@@ -161,6 +161,19 @@ int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype,
               int64_t* total_q, mux_stats_t* stats, void* stream);
 
 /*
+ * mux_match with ordering keys for the multilevel solver: rowkey_dev[n] and
+ * colkey_dev[m] (float64, DEVICE) order rows and columns by similarity -- for
+ * the table predictor the online and offline SM demands.  NULL keys fall back
+ * to row / column sums of the weights.  Same results as mux_match (the keys
+ * only steer the warm start, never the optimum).
+ */
+int mux_match_keyed(mux_ctx_t* ctx, const void* Wq_dev, int wtype,
+                    int64_t n, int64_t m, int64_t ldw,
+                    const double* rowkey_dev, const double* colkey_dev,
+                    int32_t* col_of_row_out, int out_on_host,
+                    int64_t* total_q, mux_stats_t* stats, void* stream);
+
+/*
  * One fused scheduling round from HOST feature arrays (the call the
  * reference's `_matching_policy_schedule` makes per round, scheduler.py:143-194):
  * H2D copy of (x, share, y), exact scoring into quantised weights, auction,

@@ -19,7 +19,8 @@ MUX_SCORE_EXACT, MUX_SCORE_FAST = 0, 1
 
 # every symbol include/muxflow.h declares (checked by tests/test_native_abi.py)
 EXPORTS = ("mux_version", "mux_last_error", "mux_ctx_create", "mux_ctx_destroy",
-           "mux_table_validate", "mux_score_table", "mux_score_mlp", "mux_match", "mux_round")
+           "mux_table_validate", "mux_score_table", "mux_score_mlp", "mux_match", "mux_match_keyed",
+           "mux_round")
 
 
 class MuxTable(ctypes.Structure):
@@ -81,6 +82,8 @@ def load():
         lib.mux_score_mlp.argtypes = [P, P, P, P, i64, P, i64, ctypes.c_int, ctypes.c_int, P, i64, P]
         lib.mux_match.argtypes = [P, P, ctypes.c_int, i64, i64, i64, P, ctypes.c_int,
                                   ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
+        lib.mux_match_keyed.argtypes = [P, P, ctypes.c_int, i64, i64, i64, P, P, P, ctypes.c_int,
+                                        ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         lib.mux_round.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int, P,
                                   ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         for name in EXPORTS[2:]:

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -177,6 +178,37 @@ int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t 
     if (stats) memset(stats, 0, sizeof(*stats));
     MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
                            env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1), nullptr, nullptr));
+    if (out_on_host && n > 0) {
+        MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return MUX_OK;
+}
+
+int mux_match_keyed(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t m, int64_t ldw,
+                    const double* rowkey_dev, const double* colkey_dev, int32_t* col_of_row_out, int out_on_host,
+                    int64_t* total_q, mux_stats_t* stats, void* stream) {
+    if (!ctx) { set_error("null context"); return MUX_EINVAL; }
+    if ((rowkey_dev == nullptr) != (colkey_dev == nullptr)) { set_error("mux_match_keyed: give both keys or neither"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<double> rk, ck;
+    if (rowkey_dev && n > 0 && m > 0) {
+        rk.resize(n);
+        ck.resize(m);
+        MUX_CUDA_TRY(cudaMemcpyAsync(rk.data(), rowkey_dev, 8ull * n, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(ck.data(), colkey_dev, 8ull * m, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    int32_t* col_dev = col_of_row_out;
+    if (out_on_host) {
+        MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)(n > 0 ? n : 1)));
+        col_dev = ctx->colout.as<int32_t>();
+    }
+    if (stats) memset(stats, 0, sizeof(*stats));
+    MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
+                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1),
+                           rk.empty() ? nullptr : rk.data(), ck.empty() ? nullptr : ck.data()));
     if (out_on_host && n > 0) {
         MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));

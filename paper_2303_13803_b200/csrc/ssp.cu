@@ -57,7 +57,7 @@ constexpr int TC = 256;                // touched columns per warp table (parall
 constexpr int HSZ = 512;               // hash slots per warp table
 constexpr int PWARPS = 8;              // warps per CTA in parallel mode
 constexpr int STEP_BUDGET = 192;       // Dijkstra pops before a search is deferred
-constexpr int DEEP_BUDGET = 24;        // dense re-scans before a search is deferred
+constexpr int DEEP_BUDGET = 8;         // dense row re-scans before a search is deferred
 constexpr int MAX_TRIES = 16;          // lock-conflict retries before deferral
 constexpr int64_t kDistLim = 1ll << 39;
 constexpr int64_t kInf = INT64_MAX / 4;
@@ -194,7 +194,9 @@ __device__ __forceinline__ void warp_top32(int32_t m, F keyf, uint64_t& mine, ui
 __device__ void refresh_row(const Lvl& L, int32_t i) {
     const int32_t* Ar = L.A + (int64_t)i * L.lda;
     uint64_t mine, bound;
-    warp_top32(L.m, [&](int32_t j) { return mkkey(ldv64(L.p + j) - (int64_t)__ldg(Ar + j), j, &L.cnt->errors); },
+    // plain L2 loads (pipelined): a price read late is still a price the column
+    // had, and prices only rise, so tau stays an upper bound
+    warp_top32(L.m, [&](int32_t j) { return mkkey(__ldcg(L.p + j) - (int64_t)__ldg(Ar + j), j, &L.cnt->errors); },
                mine, bound);
     const int32_t j = mine == kNoKey ? -1 : key_idx(mine);
     L.cj[(int64_t)i * KC + lane_id()] = j;
@@ -300,7 +302,7 @@ __device__ int64_t deep_relax(WTab& T, int32_t& nt, const Lvl& L, int32_t r, int
     warp_top32(L.m, [&](int32_t j) -> uint64_t {
         const int32_t e = hfind(T, j);
         if (e >= 0 && (T.st[e] & kScanned)) return kNoKey;
-        return mkkey(db + ldv64(L.p + j) - (int64_t)__ldg(Ar + j), j, &L.cnt->errors);
+        return mkkey(db + __ldcg(L.p + j) - (int64_t)__ldg(Ar + j), j, &L.cnt->errors);
     }, mine, bound);
     const int32_t c = mine == kNoKey ? -1 : key_idx(mine);
     int64_t pc = 0, nd = 0;
@@ -356,9 +358,11 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
         const int64_t dmin = best == kNoKey ? kInf : (int64_t)(best >> 24);
         if (dmin > H) {
             // horizon: re-scan every tree row whose bound is below dmin
-            if (++deeps > DEEP_BUDGET) { result = kTooBig; break; }
             bool ok = true;
-            if (hsrc < dmin) hsrc = deep_relax(T, nt, L, s, pis, ok);
+            if (hsrc < dmin) {
+                if (++deeps > DEEP_BUDGET) { result = kTooBig; break; }
+                hsrc = deep_relax(T, nt, L, s, pis, ok);
+            }
             int64_t nh = hsrc;
             for (int e0 = 0; e0 < nt && ok; e0 += 32) {
                 const int e = e0 + lane;
@@ -367,6 +371,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
                 while (bal && ok) {
                     const int src = __ffs(bal) - 1;
                     bal &= bal - 1;
+                    if (++deeps > DEEP_BUDGET) { ok = false; break; }
                     const int ee = e0 + src;
                     const int32_t r = T.row[ee];
                     const int64_t pir = (int64_t)__ldg(L.A + (int64_t)r * L.lda + T.col[ee]) - T.snap[ee];
@@ -712,86 +717,110 @@ __global__ void __launch_bounds__(32, 1) ssp_exclusive_kernel(Lvl L, int32_t nde
 // ---------------------------------------------------------------------------
 
 constexpr int DTHREADS = 1024;
+constexpr int DCOLS = 11;            // columns per thread: m <= 11264 (21 bytes of shared memory each)
 
-__device__ __forceinline__ uint64_t block_min64(uint64_t v, uint64_t* red) {
+// block-wide min; red holds two 33-entry buffers used alternately, so a
+// step needs only the two barriers inside
+__device__ __forceinline__ uint64_t block_min64(uint64_t v, uint64_t* red, int& par) {
     v = wmin64(v);
+    uint64_t* R = red + par * 33;
+    par ^= 1;
     const int w = threadIdx.x >> 5;
-    if (lane_id() == 0) red[w] = v;
+    if (lane_id() == 0) R[w] = v;
     __syncthreads();
     if (w == 0) {
-        uint64_t x = lane_id() < (DTHREADS / 32) ? red[lane_id()] : kNoKey;
+        uint64_t x = lane_id() < (DTHREADS / 32) ? R[lane_id()] : kNoKey;
         x = wmin64(x);
-        if (lane_id() == 0) red[32] = x;
+        if (lane_id() == 0) R[32] = x;
     }
     __syncthreads();
-    const uint64_t r = red[32];
-    __syncthreads();
-    return r;
+    return R[32];
 }
 
 __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t ndef) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint64_t red[33];
-    __shared__ int32_t s_own;
+    __shared__ uint64_t red[66];
     const int32_t m = L.m;
     int64_t* d = reinterpret_cast<int64_t*>(smem);
     int64_t* ps = d + m;
-    int32_t* pred = reinterpret_cast<int32_t*>(ps + m);
-    uint8_t* fl = reinterpret_cast<uint8_t*>(pred + m);   // bit0 scanned, bit1 free
+    int16_t* pred = reinterpret_cast<int16_t*>(ps + m);
+    int16_t* rocs = pred + m;
+    uint8_t* fl = reinterpret_cast<uint8_t*>(rocs + m);   // bit0 scanned, bit1 free
     const int tid = threadIdx.x;
+    int par = 0;
     unsigned long long steps = 0;
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
         const int32_t* As = L.A + (int64_t)s * L.lda;
-        uint64_t vmax = 0;   // max value via min of negated keys
-        for (int32_t j = tid; j < m; j += DTHREADS) {
-            const int64_t pj = __ldcg(L.p + j);
-            ps[j] = pj;
-            fl[j] = __ldcg(L.roc + j) < 0 ? 2 : 0;
-            const int64_t v = (int64_t)__ldg(As + j) - pj;
-            const uint64_t k = (uint64_t)(kDistLim - v);   // smaller = larger value
-            vmax = (j == tid || k < vmax) ? k : vmax;
+        uint64_t vmin = kNoKey;   // max value as the min of (2^39 - value)
+#pragma unroll
+        for (int u = 0; u < DCOLS; ++u) {
+            const int32_t j = tid + u * DTHREADS;
+            if (j < m) {
+                const int64_t pj = __ldcg(L.p + j);
+                const int32_t r = __ldcg(L.roc + j);
+                ps[j] = pj;
+                rocs[j] = (int16_t)r;
+                fl[j] = r < 0 ? 2 : 0;
+                const uint64_t k = (uint64_t)(kDistLim - ((int64_t)__ldg(As + j) - pj));
+                vmin = k < vmin ? k : vmin;
+            }
         }
-        if (tid >= m) vmax = kNoKey;
-        const int64_t pis = kDistLim - (int64_t)block_min64(vmax, red);
+        const int64_t pis = kDistLim - (int64_t)block_min64(vmin, red, par);
         uint64_t best = kNoKey;
-        for (int32_t j = tid; j < m; j += DTHREADS) {
-            const int64_t nd = pis + ps[j] - (int64_t)__ldg(As + j);
-            d[j] = nd;
-            pred[j] = s;
-            const uint64_t k = ((uint64_t)nd << 24) | ((fl[j] & 2) ? 0u : (1u << 23)) | (uint32_t)j;
-            best = k < best ? k : best;
+#pragma unroll
+        for (int u = 0; u < DCOLS; ++u) {
+            const int32_t j = tid + u * DTHREADS;
+            if (j < m) {
+                const int64_t nd = pis + ps[j] - (int64_t)__ldg(As + j);
+                d[j] = nd;
+                pred[j] = (int16_t)s;
+                const uint64_t k = ((uint64_t)nd << 24) | ((fl[j] & 2) ? 0u : (1u << 23)) | (uint32_t)j;
+                best = k < best ? k : best;
+            }
         }
-        best = block_min64(best, red);
+        best = block_min64(best, red, par);
         int32_t jf;
         int64_t D;
         while (true) {
             const int32_t jm = (int32_t)(best & 0x7FFFFFu);
             const int64_t dmin = (int64_t)(best >> 24);
             if (fl[jm] & 2) { jf = jm; D = dmin; break; }
-            if (tid == 0) { fl[jm] |= 1; s_own = __ldcg(L.roc + jm); }
-            __syncthreads();
-            const int32_t i = s_own;
+            const int32_t i = rocs[jm];
+            if ((jm & (DTHREADS - 1)) == tid) fl[jm] |= 1;   // only the column's owner thread reads its flag
             const int32_t* Ai = L.A + (int64_t)i * L.lda;
+            // the whole row slice and a_i,jm in one batch of loads
+            int32_t av[DCOLS];
+#pragma unroll
+            for (int u = 0; u < DCOLS; ++u) {
+                const int32_t j = tid + u * DTHREADS;
+                av[u] = j < m ? __ldg(Ai + j) : 0;
+            }
             const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - ps[jm];
             best = kNoKey;
-            for (int32_t j = tid; j < m; j += DTHREADS) {
-                int64_t dj = d[j];
-                const uint8_t f = fl[j];
-                if (!(f & 1)) {
-                    const int64_t nd = base + ps[j] - (int64_t)__ldg(Ai + j);
-                    if (nd < dj) { dj = nd; d[j] = nd; pred[j] = i; }
-                    const uint64_t k = ((uint64_t)dj << 24) | ((f & 2) ? 0u : (1u << 23)) | (uint32_t)j;
-                    best = k < best ? k : best;
+#pragma unroll
+            for (int u = 0; u < DCOLS; ++u) {
+                const int32_t j = tid + u * DTHREADS;
+                if (j < m) {
+                    const uint8_t f = fl[j];
+                    if (!(f & 1)) {
+                        int64_t dj = d[j];
+                        const int64_t nd = base + ps[j] - (int64_t)av[u];
+                        if (nd < dj) { dj = nd; d[j] = nd; pred[j] = (int16_t)i; }
+                        const uint64_t k = ((uint64_t)dj << 24) | ((f & 2) ? 0u : (1u << 23)) | (uint32_t)j;
+                        best = k < best ? k : best;
+                    }
                 }
             }
-            best = block_min64(best, red);
+            best = block_min64(best, red, par);
             ++steps;
         }
         // dual update on the scanned columns, then the path (thread 0)
-        for (int32_t j = tid; j < m; j += DTHREADS)
-            if ((fl[j] & 1) && j != jf) L.p[j] = ps[j] + (D - d[j]);
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < DCOLS; ++u) {
+            const int32_t j = tid + u * DTHREADS;
+            if (j < m && (fl[j] & 1)) L.p[j] = ps[j] + (D - d[j]);
+        }
         if (tid == 0) {
             int32_t j = jf;
             while (true) {
@@ -843,17 +872,33 @@ __global__ void profit_kernel(const int32_t* A, int64_t lda, int32_t m, const in
     pi[k] = (int64_t)A[(int64_t)k * lda + j] - p[j];
 }
 
-// c-transform: p_j = max_k (A[sub[k]][j] - pi_k) over the coarse rows k
+// c-transform: p_j = max_k (A[sub[k]][j] - pi_k) over the coarse rows k.
+// blockIdx.y takes one chunk of the coarse rows; partial maxima meet in an
+// atomicMax (p pre-filled with INT64_MIN).
 __global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t m, const int32_t* sub, const int64_t* pi,
-                                  int32_t mc, int64_t* p) {
+                                  int32_t mc, int32_t chunk, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
+    const int32_t k0 = blockIdx.y * chunk, k1 = min(mc, k0 + chunk);
     int64_t b = INT64_MIN;
-    for (int32_t k = 0; k < mc; ++k) {
-        const int64_t v = (int64_t)__ldg(A + (int64_t)sub[k] * lda + j) - __ldg(pi + k);
+    int32_t k = k0;
+    for (; k + 4 <= k1; k += 4) {
+        int64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (int64_t)__ldg(A + (int64_t)__ldg(sub + k + u) * lda + j) - __ldg(pi + k + u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) b = v[u] > b ? v[u] : b;
+    }
+    for (; k < k1; ++k) {
+        const int64_t v = (int64_t)__ldg(A + (int64_t)__ldg(sub + k) * lda + j) - __ldg(pi + k);
         b = v > b ? v : b;
     }
-    p[j] = b;
+    if (b != INT64_MIN) atomicMax(reinterpret_cast<long long*>(p + j), (long long)b);
+}
+
+__global__ void fill_i64_kernel(int64_t* p, int32_t m, int64_t v) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < m) p[j] = v;
 }
 
 __global__ void init_level_kernel(int32_t m, int32_t* cor, int32_t* roc, int32_t* lock, int32_t* tries,
@@ -1072,11 +1117,20 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             profit_kernel<<<(unsigned)((mc + 255) / 256), 256, 0, st>>>(
                 reinterpret_cast<const int32_t*>(B + o_A[l + 1]), mc, mc, reinterpret_cast<int32_t*>(B + o_cor[l + 1]),
                 reinterpret_cast<int64_t*>(B + o_p[l + 1]), pic);
-            ctransform_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, m, reinterpret_cast<int32_t*>(B + o_sub[l]), pic, mc, L.p);
-            launches += 2;
+            fill_i64_kernel<<<g1, 256, 0, st>>>(L.p, m, INT64_MIN);
+            const int32_t ksplit = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * 8 / g1, mc / 64));
+            const int32_t chunk = (mc + ksplit - 1) / ksplit;
+            ctransform_kernel<<<dim3(g1, (unsigned)((mc + chunk - 1) / chunk)), 256, 0, st>>>(
+                L.A, L.lda, m, reinterpret_cast<int32_t*>(B + o_sub[l]), pic, mc, chunk, L.p);
+            launches += 3;
         }
         cand_kernel<<<(unsigned)std::min<int64_t>(((int64_t)m * 32 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(L);
         launches += 3;
+        double ms_setup = 0;
+        if (verbose) {
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            ms_setup = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
+        }
         // parallel passes
         const int32_t* list = in0;
         int32_t nlist = m;
@@ -1091,10 +1145,16 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             MUX_CUDA_TRY(cudaMemsetAsync(cnt, 0, 3 * sizeof(int32_t), st));
             const unsigned grid = (unsigned)std::min<int64_t>((int64_t)ctx->num_sms * per_sm,
                                                               ((int64_t)nlist + PWARPS - 1) / PWARPS);
-            ssp_parallel_kernel<<<grid, PWARPS * 32, psmem, st>>>(L, serial);
+            const auto tp = std::chrono::steady_clock::now();
+            // a handful of rows left: one warp, so they cannot keep aborting each other
+            ssp_parallel_kernel<<<grid, PWARPS * 32, psmem, st>>>(L, serial || nlist <= 4);
             ++launches;
             MUX_CUDA_TRY(cudaMemcpyAsync(&hc, cnt, sizeof(Cnt), cudaMemcpyDeviceToHost, st));
             MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            if (verbose && l <= 1)
+                fprintf(stderr, "[ssp]   pass %d: %d rows, grid %u, %.3f ms -> retry %d defer %d\n", pass, nlist, grid,
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp).count(),
+                        hc.nretry, hc.ndefer);
             ndef_total += hc.ndefer;
             list = L.retry;
             nlist = hc.nretry;
@@ -1105,7 +1165,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         if (ndef_total > 0) {
             L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
             const size_t dense_bytes = 21ull * m + 64;
-            if (dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
+            if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
                 // long searches: dense Dijkstra on one CTA, tables in shared memory
                 ssp_dense_kernel<<<1, DTHREADS, dense_bytes, st>>>(L, ndef_total);
             } else {
@@ -1141,9 +1201,9 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         }
         ms_levels[l] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
         if (verbose)
-            fprintf(stderr, "[ssp] level %d m %d: %.3f ms (parallel %.3f) passes %d deferred %d | steps %llu deep %llu aborts %llu "
+            fprintf(stderr, "[ssp] level %d m %d: %.3f ms (setup %.3f parallel %.3f) passes %d deferred %d | steps %llu deep %llu aborts %llu "
                             "augs %llu xsteps %llu xdeep %llu refresh %llu | xcyc pop %.2e deep %.2e step %.2e aug %.2e\n",
-                    l, m, ms_levels[l], ms_par, pass, ndef_total, hc.steps, hc.deep, hc.aborts, hc.augs, hc.xsteps, hc.xdeep,
+                    l, m, ms_levels[l], ms_setup, ms_par, pass, ndef_total, hc.steps, hc.deep, hc.aborts, hc.augs, hc.xsteps, hc.xdeep,
                     hc.refresh, (double)hc.xcyc[0], (double)hc.xcyc[1], (double)hc.xcyc[2], (double)hc.xcyc[3]);
     }
     // level 0 result
