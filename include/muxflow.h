@@ -99,6 +99,14 @@ typedef struct {
     int64_t canon_searches;  /* alternating-path searches it ran           */
     int64_t tight_edges;     /* tight edges of the real rows               */
     int64_t dual_sweeps;     /* Bellman-Ford sweeps of the exact-dual repair */
+    /* multilevel shortest-path solver (csrc/ssp.cu) */
+    int64_t levels;          /* coarse-to-fine levels solved               */
+    int64_t par_steps;       /* Dijkstra pops of the parallel warp searches */
+    int64_t dense_steps;     /* pops of the single-CTA dense searches       */
+    int64_t dense_searches;  /* searches handed to the dense kernel         */
+    double  ms_dense;        /* device time of the dense kernel (events)    */
+    double  ms_parallel;     /* device time of the parallel passes (events) */
+    double  dense_bytes;     /* weight-row bytes the dense kernel read (4 m per pop) */
 } mux_stats_t;
 
 typedef struct mux_ctx mux_ctx_t;

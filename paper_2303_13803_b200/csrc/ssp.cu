@@ -1078,6 +1078,11 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     if (per_sm < 1) { set_error("ssp kernel cannot be resident"); return MUX_ECUDA; }
     int64_t launches = 0;
     Cnt hc{};
+    cudaEvent_t ev[4];
+    for (auto& e : ev) MUX_CUDA_TRY(cudaEventCreate(&e));
+    double ms_dense = 0, ms_par = 0, dense_bytes = 0;
+    int64_t dense_searches = 0;
+    unsigned long long xsteps_prev = 0;
     double ms_levels[64] = {0};
     for (int l = nl - 1; l >= 0; --l) {
         auto tl = std::chrono::steady_clock::now();
@@ -1137,6 +1142,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         int32_t* bufs[2] = {L.retry, reinterpret_cast<int32_t*>(B + o_pi[l])};   // pi scratch doubles as 2nd retry list
         int pass = 0;
         int32_t ndef_total = 0;
+        MUX_CUDA_TRY(cudaEventRecord(ev[0], st));
         while (nlist > 0) {
             L.in = list;
             L.nin = nlist;
@@ -1161,7 +1167,9 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             ++pass;
             if (pass > 256) { set_error("ssp: retry passes exceeded"); return MUX_ELIMIT; }
         }
-        const double ms_par = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
+        MUX_CUDA_TRY(cudaEventRecord(ev[1], st));
+        const double ms_par_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
+        MUX_CUDA_TRY(cudaEventRecord(ev[2], st));
         if (ndef_total > 0) {
             L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
             const size_t dense_bytes = 21ull * m + 64;
@@ -1177,9 +1185,20 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             }
             ++launches;
         }
+        MUX_CUDA_TRY(cudaEventRecord(ev[3], st));
         MUX_CUDA_TRY(cudaGetLastError());
         MUX_CUDA_TRY(cudaMemcpyAsync(&hc, cnt, sizeof(Cnt), cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));
+        {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, ev[0], ev[1]);
+            cudaEventElapsedTime(&b, ev[2], ev[3]);
+            ms_par += a;
+            ms_dense += b;
+            dense_bytes += 4.0 * (double)m * (double)(hc.xsteps - xsteps_prev);
+            xsteps_prev = hc.xsteps;
+            dense_searches += ndef_total;
+        }
         if (hc.errors) {
             set_error(std::string("ssp: device error flags ") + std::to_string(hc.errors));
             return MUX_ELIMIT;
@@ -1203,7 +1222,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         if (verbose)
             fprintf(stderr, "[ssp] level %d m %d: %.3f ms (setup %.3f parallel %.3f) passes %d deferred %d | steps %llu deep %llu aborts %llu "
                             "augs %llu xsteps %llu xdeep %llu refresh %llu | xcyc pop %.2e deep %.2e step %.2e aug %.2e\n",
-                    l, m, ms_levels[l], ms_setup, ms_par, pass, ndef_total, hc.steps, hc.deep, hc.aborts, hc.augs, hc.xsteps, hc.xdeep,
+                    l, m, ms_levels[l], ms_setup, ms_par_wall, pass, ndef_total, hc.steps, hc.deep, hc.aborts, hc.augs, hc.xsteps, hc.xdeep,
                     hc.refresh, (double)hc.xcyc[0], (double)hc.xcyc[1], (double)hc.xcyc[2], (double)hc.xcyc[3]);
     }
     // level 0 result
@@ -1231,7 +1250,16 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         stats->ms_match = ms;
         stats->ms_kernel = ms;
         stats->launches += launches;
+        stats->levels = nl;
+        stats->par_steps = (int64_t)hc.steps;
+        stats->dense_steps = (int64_t)hc.xsteps;
+        stats->dense_searches = dense_searches;
+        stats->ms_dense = ms_dense;
+        stats->ms_parallel = ms_par;
+        stats->dense_bytes = dense_bytes;
     }
-    if (verbose) fprintf(stderr, "[ssp] n %d levels %d total %.3f ms (host wall)\n", n, nl, ms);
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (verbose) fprintf(stderr, "[ssp] n %d levels %d total %.3f ms (host wall), dense %.3f ms, parallel %.3f ms\n", n, nl, ms,
+                         ms_dense, ms_par);
     return MUX_OK;
 }
