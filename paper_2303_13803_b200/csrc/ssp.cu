@@ -47,7 +47,11 @@
 #include <numeric>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mux {
 namespace ssp {
@@ -839,6 +843,153 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
 }
 
 // ---------------------------------------------------------------------------
+// cluster mode for the long searches: the same dense Dijkstra spread over a
+// thread-block cluster of CL CTAs (CL SMs).  CTA r owns columns
+// [r*mc, (r+1)*mc); prices and column owners are replicated in every CTA's
+// shared memory (constant during a search).  Each step every warp publishes
+// its minimum key in its CTA's slot array, one cluster barrier makes all
+// slots visible, and warp 0 of every CTA reads the CL*32 slots through
+// distributed shared memory (ld.shared::cluster).  Slots are double-buffered
+// by step parity, so a step costs one cluster barrier and one CTA barrier.
+// ---------------------------------------------------------------------------
+
+constexpr int CL = 8;
+constexpr int CTHREADS = 1024;
+constexpr int CCOLS = 2;            // local columns per thread: m <= CL * CTHREADS * CCOLS
+
+__device__ __forceinline__ uint64_t cluster_min64(uint64_t v, uint64_t (*slots)[32], uint64_t* bc, int& par,
+                                                  cg::cluster_group& cluster) {
+    v = wmin64(v);
+    const int w = threadIdx.x >> 5;
+    if (lane_id() == 0) slots[par][w] = v;
+    cluster.sync();
+    if (w == 0) {
+        uint64_t x = kNoKey;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) {
+            const uint64_t* rs = cluster.map_shared_rank(&slots[par][0], r);
+            const uint64_t y = rs[lane_id()];
+            x = y < x ? y : x;
+        }
+        x = wmin64(x);
+        if (lane_id() == 0) bc[par] = x;
+    }
+    __syncthreads();
+    const uint64_t r = bc[par];
+    par ^= 1;
+    return r;
+}
+
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t slots[2][32];
+    __shared__ uint64_t bc[2];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int32_t m = L.m;
+    const int32_t mc = (m + CL - 1) / CL;
+    const int rank = (int)cluster.block_rank();
+    const int32_t c0 = rank * mc;
+    const int32_t nloc = max(0, min(mc, m - c0));
+    int64_t* ps = reinterpret_cast<int64_t*>(smem);            // [m] replica
+    int64_t* d = ps + m;                                       // [mc] local
+    int16_t* rocs = reinterpret_cast<int16_t*>(d + mc);        // [m] replica
+    int16_t* pred = rocs + m;                                  // [mc] local
+    uint8_t* fl = reinterpret_cast<uint8_t*>(pred + mc);       // [mc] local: bit0 scanned
+    const int tid = threadIdx.x;
+    int par = 0;
+    unsigned long long steps = 0;
+    for (int32_t q = 0; q < ndef; ++q) {
+        const int32_t s = L.defer[q];
+        const int32_t* As = L.A + (int64_t)s * L.lda;
+        for (int32_t j = tid; j < m; j += CTHREADS) {
+            ps[j] = __ldcg(L.p + j);
+            rocs[j] = (int16_t)__ldcg(L.roc + j);
+        }
+        __syncthreads();
+        uint64_t vmin = kNoKey;
+#pragma unroll
+        for (int u = 0; u < CCOLS; ++u) {
+            const int32_t jj = tid + u * CTHREADS;
+            if (jj < nloc) {
+                const uint64_t k = (uint64_t)(kDistLim - ((int64_t)__ldg(As + c0 + jj) - ps[c0 + jj]));
+                vmin = k < vmin ? k : vmin;
+            }
+        }
+        const int64_t pis = kDistLim - (int64_t)cluster_min64(vmin, slots, bc, par, cluster);
+        uint64_t best = kNoKey;
+#pragma unroll
+        for (int u = 0; u < CCOLS; ++u) {
+            const int32_t jj = tid + u * CTHREADS;
+            if (jj < nloc) {
+                const int32_t j = c0 + jj;
+                const int64_t nd = pis + ps[j] - (int64_t)__ldg(As + j);
+                d[jj] = nd;
+                pred[jj] = (int16_t)s;
+                fl[jj] = 0;
+                const uint64_t k = ((uint64_t)nd << 24) | (rocs[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                best = k < best ? k : best;
+            }
+        }
+        best = cluster_min64(best, slots, bc, par, cluster);
+        int32_t jf;
+        int64_t D;
+        while (true) {
+            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
+            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t i = rocs[jm];
+            if (i < 0) { jf = jm; D = dmin; break; }
+            if (jm >= c0 && jm < c0 + nloc && ((jm - c0) & (CTHREADS - 1)) == tid) fl[jm - c0] |= 1;
+            const int32_t* Ai = L.A + (int64_t)i * L.lda;
+            int32_t av[CCOLS];
+#pragma unroll
+            for (int u = 0; u < CCOLS; ++u) {
+                const int32_t jj = tid + u * CTHREADS;
+                av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
+            }
+            const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - ps[jm];
+            best = kNoKey;
+#pragma unroll
+            for (int u = 0; u < CCOLS; ++u) {
+                const int32_t jj = tid + u * CTHREADS;
+                if (jj < nloc && !(fl[jj] & 1)) {
+                    const int32_t j = c0 + jj;
+                    int64_t dj = d[jj];
+                    const int64_t nd = base + ps[j] - (int64_t)av[u];
+                    if (nd < dj) { dj = nd; d[jj] = nd; pred[jj] = (int16_t)i; }
+                    const uint64_t k = ((uint64_t)dj << 24) | (rocs[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                    best = k < best ? k : best;
+                }
+            }
+            best = cluster_min64(best, slots, bc, par, cluster);
+            ++steps;
+        }
+        // dual update on the local scanned columns
+#pragma unroll
+        for (int u = 0; u < CCOLS; ++u) {
+            const int32_t jj = tid + u * CTHREADS;
+            if (jj < nloc && (fl[jj] & 1)) L.p[c0 + jj] = ps[c0 + jj] + (D - d[jj]);
+        }
+        // the path: predecessors live in their owners' shared memory
+        if (rank == 0 && tid == 0) {
+            int32_t j = jf;
+            while (true) {
+                const int owner = j / mc;
+                const int16_t* pr = cluster.map_shared_rank(pred, owner);
+                const int32_t i = pr[j - owner * mc];
+                const int32_t jn = (i == s) ? -1 : __ldcg(L.cor + i);
+                L.roc[j] = i;
+                L.cor[i] = j;
+                if (i == s) break;
+                j = jn;
+            }
+        }
+        __threadfence();
+        cluster.sync();
+    }
+    if (rank == 0 && tid == 0) atomicAdd(&L.cnt->xsteps, steps);
+}
+
+// ---------------------------------------------------------------------------
 // level setup kernels
 // ---------------------------------------------------------------------------
 
@@ -1073,6 +1224,8 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_parallel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_exclusive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    const bool use_cluster = !(getenv("MUX_SSP_CLUSTER") && *getenv("MUX_SSP_CLUSTER") == '0');
     int per_sm = 0;
     MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssp_parallel_kernel, PWARPS * 32, psmem));
     if (per_sm < 1) { set_error("ssp kernel cannot be resident"); return MUX_ECUDA; }
@@ -1173,7 +1326,12 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         if (ndef_total > 0) {
             L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
             const size_t dense_bytes = 21ull * m + 64;
-            if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
+            const int32_t mcl = (m + CL - 1) / CL;
+            const size_t cl_bytes = 10ull * m + 11ull * mcl + 64;
+            if (use_cluster && m <= CL * CTHREADS * CCOLS && m < 32768 && cl_bytes <= xs_budget - 1024) {
+                // long searches: dense Dijkstra over a cluster of CL SMs
+                ssp_cluster_kernel<<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total);
+            } else if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
                 // long searches: dense Dijkstra on one CTA, tables in shared memory
                 ssp_dense_kernel<<<1, DTHREADS, dense_bytes, st>>>(L, ndef_total);
             } else {
