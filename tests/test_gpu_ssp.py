@@ -1,0 +1,167 @@
+"""GPU parity of the multilevel shortest-path solver (csrc/ssp.cu), the
+default matcher for square int32 problems.  Oracles: scipy's exact LSA
+(cross-checked against the reference's Hungarian on dyadic weights, SURVEY.md
+Appendix A) and the oracle's C restatement of matching.py:45-101.  With
+MUX_SSP_CHECK=1 the library also verifies the dense dual certificate
+pi_i + p_j >= a_ij (tight on the matching) at every level, which proves
+optimality independently of any oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import matching_ref, predictor_ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _match(Q, keys=None, stats=False):
+    import torch
+    from paper_2303_13803_b200 import _native as nat
+    n, m = Q.shape
+    ldw = max(4, (m + 3) // 4 * 4)
+    P = np.zeros((n, ldw), dtype=np.int32)
+    P[:, :m] = Q
+    Wq = torch.as_tensor(P, device="cuda")
+    col = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    total = nat.ctypes.c_int64(0)
+    st = nat.MuxStats()
+    if keys is None:
+        rk = ck = None
+        rp = cp = None
+    else:
+        rk = torch.as_tensor(np.asarray(keys[0], dtype=np.float64), device="cuda")
+        ck = torch.as_tensor(np.asarray(keys[1], dtype=np.float64), device="cuda")
+        rp, cp = rk.data_ptr(), ck.data_ptr()
+    nat.check(nat.load().mux_match_keyed(nat.context(0), Wq.data_ptr(), nat.MUX_W_I32, n, m, ldw, rp, cp,
+                                         col.data_ptr(), 0, nat.ctypes.byref(total), nat.ctypes.byref(st),
+                                         nat.stream_ptr()))
+    out = col[:n].cpu().numpy(), int(total.value)
+    return out + (st.as_dict(),) if stats else out
+
+
+def _lsa(Q):
+    from scipy.optimize import linear_sum_assignment
+    r, c = linear_sum_assignment(Q.astype(np.float64), maximize=True)
+    return int(Q[r, c].sum())
+
+
+def _pred_Q(n, seed, qbits):
+    from paper_2303_13803_b200 import default_table
+    from paper_2303_13803_b200.synth import make_cluster
+    t = default_table()
+    cl = make_cluster(n, n, seed=seed)
+    W = predictor_ref.predict_pairs_exact(t.axes, t.values, cl.x, cl.share, cl.y)
+    return cl, np.rint(np.where(W >= 1e-6, W, 0.0) * 2.0 ** qbits).astype(np.int64)
+
+
+def _check_assignment(Q, col, total):
+    used = col[col >= 0]
+    assert len(np.unique(used)) == len(used)
+    assert matching_ref.assignment_total_int(Q, col) == total
+
+
+@pytest.fixture
+def certified(monkeypatch):
+    monkeypatch.setenv("MUX_SSP_CHECK", "1")
+
+
+@pytest.mark.parametrize("n,hi,seed", [(2, 5, 0), (7, 100, 1), (33, 3, 2), (50, 1 << 20, 3), (129, 2, 4),
+                                       (300, 1000, 5), (777, 50, 6), (1000, 1 << 30, 7)])
+def test_random_matrices_vs_lsa(cuda, certified, n, hi, seed):
+    """Uniform integer weights, including heavily tied ones (hi = 2, 3)."""
+    Q = np.random.default_rng(seed).integers(1, hi, size=(n, n)).astype(np.int64)
+    col, total = _match(Q)
+    assert total == _lsa(Q)
+    _check_assignment(Q, col, total)
+
+
+@pytest.mark.parametrize("n,q,seed", [(64, 20, 0), (400, 20, 1), (1000, 30, 2), (1500, 24, 3), (2048, 30, 4)])
+def test_predictor_rounds_vs_lsa(cuda, certified, n, q, seed):
+    """Predictor-derived (near rank-1, degenerate) weights, keyed by the SM demands."""
+    cl, Q = _pred_Q(n, seed, q)
+    col, total = _match(Q, keys=(cl.x, cl.y))
+    assert total == _lsa(Q)
+    _check_assignment(Q, col, total)
+
+
+def test_keys_only_steer_the_warm_start(cuda, certified):
+    """Feature keys, row/column-sum keys and adversarial (reversed) keys give the same optimum."""
+    cl, Q = _pred_Q(900, 11, 30)
+    want = _lsa(Q)
+    for keys in ((cl.x, cl.y), None, (-cl.x, cl.y[::-1].copy()), (np.zeros(900), np.zeros(900))):
+        col, total = _match(Q, keys=keys)
+        assert total == want
+        _check_assignment(Q, col, total)
+
+
+def test_matches_the_oracle_hungarian(cuda, certified):
+    """The oracle's C restatement of the reference Kuhn-Munkres on the same integers."""
+    for n, q, seed in ((256, 30, 20), (500, 16, 21)):
+        _, Q = _pred_Q(n, seed, q)
+        want, _ = matching_ref.max_weight_total_int(Q)
+        _, total = _match(Q)
+        assert total == want
+
+
+def test_auction_and_ssp_agree(cuda, monkeypatch):
+    """The two GPU solvers (MUX_SOLVER=auction vs the default) reach the same optimum."""
+    _, Q = _pred_Q(700, 22, 20)
+    _, t_ssp = _match(Q)
+    monkeypatch.setenv("MUX_SOLVER", "auction")
+    _, t_auc = _match(Q)
+    assert t_ssp == t_auc == _lsa(Q)
+
+
+@pytest.mark.parametrize("f,base", [("2", "48"), ("4", "48"), ("2", "8"), ("3", "200")])
+def test_level_structure_variants(cuda, certified, monkeypatch, f, base):
+    """Coarsening factor and base size change only the work, never the optimum."""
+    monkeypatch.setenv("MUX_SSP_F", f)
+    monkeypatch.setenv("MUX_SSP_BASE", base)
+    cl, Q = _pred_Q(1200, 30, 30)
+    _, total = _match(Q, keys=(cl.x, cl.y))
+    assert total == _lsa(Q)
+
+
+def test_long_path_kernels_agree(cuda, certified, monkeypatch):
+    """Cluster (default), single-CTA dense and single-warp sparse long-path modes."""
+    cl, Q = _pred_Q(1800, 31, 30)
+    want = _lsa(Q)
+    for env in ({}, {"MUX_SSP_CLUSTER": "0"}, {"MUX_SSP_CLUSTER": "0", "MUX_SSP_SPARSEX": "1"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        _, total = _match(Q, keys=(cl.x, cl.y))
+        assert total == want, env
+
+
+def test_serial_and_parallel_searches_agree(cuda, certified, monkeypatch):
+    """Lock-based concurrent warp searches vs one search at a time."""
+    cl, Q = _pred_Q(1000, 40, 30)
+    _, t_par = _match(Q, keys=(cl.x, cl.y))
+    monkeypatch.setenv("MUX_SSP_SERIAL", "1")
+    _, t_ser = _match(Q, keys=(cl.x, cl.y))
+    assert t_par == t_ser == _lsa(Q)
+
+
+@pytest.mark.slow
+def test_certificate_at_4k_many_seeds(cuda, certified):
+    """Dense dual certificate at every level, 4k x 4k, several snapshots."""
+    from paper_2303_13803_b200 import default_table, round_arrays
+    from paper_2303_13803_b200.synth import make_cluster
+    t = default_table()
+    totals = []
+    for seed in range(3):
+        cl = make_cluster(4000, 4000, seed=seed)
+        col, total, st = round_arrays(t, cl.x, cl.share, cl.y, qbits=30, stats=True)
+        assert st["levels"] >= 2
+        assert (col >= 0).all()
+        totals.append(total)
+    assert len(set(totals)) == 3
+
+
+def test_stats_reported(cuda):
+    cl, Q = _pred_Q(1500, 50, 30)
+    _, total, st = _match(Q, keys=(cl.x, cl.y), stats=True)
+    assert st["total_q"] == total
+    assert st["levels"] >= 3
+    assert st["par_steps"] > 0
+    assert st["ms_parallel"] > 0
