@@ -60,8 +60,8 @@ constexpr int KC = 32;                 // candidates per row record (one per lan
 constexpr int TC = 256;                // touched columns per warp table (parallel mode)
 constexpr int HSZ = 512;               // hash slots per warp table
 constexpr int PWARPS = 8;              // warps per CTA in parallel mode
-constexpr int STEP_BUDGET = 192;       // Dijkstra pops before a search is deferred
-constexpr int DEEP_BUDGET = 8;         // dense row re-scans before a search is deferred
+constexpr int STEP_BUDGET_DEFAULT = 48;   // Dijkstra pops before a search is deferred
+constexpr int DEEP_BUDGET_DEFAULT = 4;    // dense row re-scans before a search is deferred
 constexpr int MAX_TRIES = 16;          // lock-conflict retries before deferral
 constexpr int64_t kDistLim = 1ll << 39;
 constexpr int64_t kInf = INT64_MAX / 4;
@@ -99,6 +99,8 @@ struct Lvl {
     int32_t* defer;     // rows for the exclusive pass
     int32_t* tries;     // [m]
     Cnt* cnt;
+    int32_t step_budget;
+    int32_t deep_budget;
     // exclusive-mode scratch (global, direct-indexed by column)
     int64_t* xdist;
     int32_t* xpred;
@@ -364,7 +366,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
             // horizon: re-scan every tree row whose bound is below dmin
             bool ok = true;
             if (hsrc < dmin) {
-                if (++deeps > DEEP_BUDGET) { result = kTooBig; break; }
+                if (++deeps > L.deep_budget) { result = kTooBig; break; }
                 hsrc = deep_relax(T, nt, L, s, pis, ok);
             }
             int64_t nh = hsrc;
@@ -375,7 +377,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
                 while (bal && ok) {
                     const int src = __ffs(bal) - 1;
                     bal &= bal - 1;
-                    if (++deeps > DEEP_BUDGET) { ok = false; break; }
+                    if (++deeps > L.deep_budget) { ok = false; break; }
                     const int ee = e0 + src;
                     const int32_t r = T.row[ee];
                     const int64_t pir = (int64_t)__ldg(L.A + (int64_t)r * L.lda + T.col[ee]) - T.snap[ee];
@@ -421,7 +423,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
             continue;
         }
         if (own < 0) { jf = cc; ef = e; D = dmin; result = kDone; break; }
-        if (++steps > STEP_BUDGET) { result = kTooBig; break; }
+        if (++steps > L.step_budget) { result = kTooBig; break; }
         const int64_t pir = (int64_t)__ldg(L.A + (int64_t)own * L.lda + cc) - pnow;
         if (lane == 0) { T.st[e] |= kScanned; T.row[e] = own; }
         __syncwarp();
@@ -880,7 +882,7 @@ __device__ __forceinline__ uint64_t cluster_min64(uint64_t v, uint64_t (*slots)[
     return r;
 }
 
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef) {
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t slots[2][32];
     __shared__ uint64_t bc[2];
@@ -933,11 +935,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
         best = cluster_min64(best, slots, bc, par, cluster);
         int32_t jf;
         int64_t D;
+        int32_t pops = 0;
+        bool abandon = false;
         while (true) {
             const int32_t jm = (int32_t)(best & 0x7FFFFFu);
             const int64_t dmin = (int64_t)(best >> 24);
             const int32_t i = rocs[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
+            // coarse levels: a search past the pop limit is abandoned (row stays free)
+            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             if (jm >= c0 && jm < c0 + nloc && ((jm - c0) & (CTHREADS - 1)) == tid) fl[jm - c0] |= 1;
             const int32_t* Ai = L.A + (int64_t)i * L.lda;
             int32_t av[CCOLS];
@@ -963,6 +969,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
             best = cluster_min64(best, slots, bc, par, cluster);
             ++steps;
         }
+        if (abandon) { cluster.sync(); continue; }
         // dual update on the local scanned columns
 #pragma unroll
         for (int u = 0; u < CCOLS; ++u) {
@@ -1014,13 +1021,25 @@ __global__ void colmax_kernel(const int32_t* A, int64_t lda, int32_t m, int64_t*
     p[j] = b;
 }
 
-// pi_k = a_k,cor(k) - p_cor(k) of a solved level
+// pi_k of a solved level: a_k,cor(k) - p_cor(k) for matched rows; rows a
+// coarse level left unmatched (its long searches are skipped) take the
+// dual-feasible max_j (a_kj - p_j).  One warp per row.
 __global__ void profit_kernel(const int32_t* A, int64_t lda, int32_t m, const int32_t* cor, const int64_t* p,
                               int64_t* pi) {
-    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t k = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     if (k >= m) return;
     const int32_t j = cor[k];
-    pi[k] = (int64_t)A[(int64_t)k * lda + j] - p[j];
+    if (j >= 0) {
+        if (lane_id() == 0) pi[k] = (int64_t)A[(int64_t)k * lda + j] - p[j];
+        return;
+    }
+    int64_t b = -kInf;
+    for (int32_t c = lane_id(); c < m; c += 32) {
+        const int64_t v = (int64_t)A[(int64_t)k * lda + c] - p[c];
+        b = v > b ? v : b;
+    }
+    b = wmax64s(b);
+    if (lane_id() == 0) pi[k] = b;
 }
 
 // c-transform: p_j = max_k (A[sub[k]][j] - pi_k) over the coarse rows k.
@@ -1132,6 +1151,11 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     const int base = std::max(8, atoi(getenv("MUX_SSP_BASE") ? getenv("MUX_SSP_BASE") : "48"));
     const bool check = getenv("MUX_SSP_CHECK") && *getenv("MUX_SSP_CHECK") == '1';
     const int32_t serial = getenv("MUX_SSP_SERIAL") && *getenv("MUX_SSP_SERIAL") == '1';
+    const int32_t step_budget = getenv("MUX_SSP_STEPS") ? atoi(getenv("MUX_SSP_STEPS")) : STEP_BUDGET_DEFAULT;
+    const int32_t deep_budget = getenv("MUX_SSP_DEEP") ? atoi(getenv("MUX_SSP_DEEP")) : DEEP_BUDGET_DEFAULT;
+    // pop limit of the long searches at coarse levels (0 = exact coarse levels)
+    const int32_t coarse_pops = getenv("MUX_SSP_COARSE_POPS") ? atoi(getenv("MUX_SSP_COARSE_POPS")) : 0;
+    const bool coarse_exact = coarse_pops == 0;
     auto t0 = std::chrono::steady_clock::now();
 
     // ordering keys -> sorted index lists
@@ -1255,6 +1279,8 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
         L.tries = reinterpret_cast<int32_t*>(B + o_tr[l]);
         L.cnt = cnt;
+        L.step_budget = step_budget;
+        L.deep_budget = deep_budget;
         L.xdist = reinterpret_cast<int64_t*>(B + o_xd);
         L.xpred = reinterpret_cast<int32_t*>(B + o_xp);
         L.xstamp = reinterpret_cast<int32_t*>(B + o_xs);
@@ -1272,7 +1298,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         } else {
             const int32_t mc = lv[l + 1].m;
             int64_t* pic = reinterpret_cast<int64_t*>(B + o_pi[l + 1]);
-            profit_kernel<<<(unsigned)((mc + 255) / 256), 256, 0, st>>>(
+            profit_kernel<<<(unsigned)(((int64_t)mc * 32 + 255) / 256), 256, 0, st>>>(
                 reinterpret_cast<const int32_t*>(B + o_A[l + 1]), mc, mc, reinterpret_cast<int32_t*>(B + o_cor[l + 1]),
                 reinterpret_cast<int64_t*>(B + o_p[l + 1]), pic);
             fill_i64_kernel<<<g1, 256, 0, st>>>(L.p, m, INT64_MIN);
@@ -1323,6 +1349,8 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         MUX_CUDA_TRY(cudaEventRecord(ev[1], st));
         const double ms_par_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
         MUX_CUDA_TRY(cudaEventRecord(ev[2], st));
+        // coarse levels only supply warm duals: their long searches are skipped
+        // (the partial assignment with its duals is feasible and near-optimal)
         if (ndef_total > 0) {
             L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
             const size_t dense_bytes = 21ull * m + 64;
@@ -1330,7 +1358,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             const size_t cl_bytes = 10ull * m + 11ull * mcl + 64;
             if (use_cluster && m <= CL * CTHREADS * CCOLS && m < 32768 && cl_bytes <= xs_budget - 1024) {
                 // long searches: dense Dijkstra over a cluster of CL SMs
-                ssp_cluster_kernel<<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total);
+                ssp_cluster_kernel<<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, l == 0 ? 0 : coarse_pops);
             } else if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
                 // long searches: dense Dijkstra on one CTA, tables in shared memory
                 ssp_dense_kernel<<<1, DTHREADS, dense_bytes, st>>>(L, ndef_total);
@@ -1361,7 +1389,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             set_error(std::string("ssp: device error flags ") + std::to_string(hc.errors));
             return MUX_ELIMIT;
         }
-        if (check) {
+        if (check && (l == 0 || coarse_exact)) {
             unsigned long long* bad = reinterpret_cast<unsigned long long*>(B + o_tot);
             MUX_CUDA_TRY(cudaMemsetAsync(bad, 0, 32, st));
             check_kernel<<<m, 256, 0, st>>>(L.A, L.lda, m, L.cor, L.roc, L.p, bad);
