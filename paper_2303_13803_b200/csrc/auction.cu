@@ -1335,11 +1335,12 @@ __global__ void finalize_kernel(const void* W, int64_t ldw, int32_t N, int32_t M
     if ((threadIdx.x & 31) == 0 && q) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->total_q), (unsigned long long)q);
 }
 
-__global__ void finalize_ssp_kernel(const int32_t* W, int64_t ldw, int32_t n, const int32_t* col, int32_t* out) {
+__global__ void finalize_ssp_kernel(const int32_t* W, int64_t ldw, int32_t N, int32_t M, const int32_t* col,
+                                    int32_t* out) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) {
+    if (i < N) {
         const int32_t j = col[i];
-        out[i] = (j >= 0 && j < n && W[(int64_t)i * ldw + j] > 0) ? j : -1;
+        out[i] = (j >= 0 && j < M && W[(int64_t)i * ldw + j] > 0) ? j : -1;
     }
 }
 
@@ -1362,7 +1363,7 @@ static int env_flag(const char* name, int dflt) {
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const double* rowkey,
+int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
                  int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st);
 
@@ -1391,9 +1392,13 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         // Square int32 problems: multilevel shortest-path solver (csrc/ssp.cu);
         // MUX_SOLVER=auction selects the epsilon-scaling auction below.
         const char* sv = getenv("MUX_SOLVER");
-        const bool use_ssp = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && N == M && N >= 2;
+        // N < M: the zero padding rows of the reference's square problem are
+        // implicit; N > M (more online rows than jobs) stays on the auction
+        const bool rect_ok = !(getenv("MUX_SSP_RECT") && *getenv("MUX_SSP_RECT") == '0');
+        const bool use_ssp = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && N >= 1 && M >= 2 &&
+                             (N == M || (N < M && rect_ok));
         if (use_ssp) {
-            const int32_t nn = (int32_t)N;
+            const int32_t nn = (int32_t)M;
             const size_t o_p = 0, o_c = (8ull * nn + 255) & ~255ull, o_o = o_c + ((4ull * nn + 255) & ~255ull);
             MUX_TRY(ctx->auc.ensure(o_o + 4ull * nn + 256));
             char* base = ctx->auc.as<char>();
@@ -1401,16 +1406,17 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             int32_t* colr = reinterpret_cast<int32_t*>(base + o_c);
             int32_t* owner = reinterpret_cast<int32_t*>(base + o_o);
             int64_t tq = 0;
-            MUX_TRY(mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, nn, rowkey, colkey, col_out_dev, &tq,
-                                 price, colr, owner, stats, st));
+            MUX_TRY(mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, rowkey, colkey, col_out_dev,
+                                 &tq, price, colr, owner, stats, st));
             const char* cs = getenv("MUX_CANON");
             if (!(cs && *cs == '0')) {
                 // canonicalisation works in the auction's units: benefits Q * (n + 1)
                 scale_price_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(price, nn, (int64_t)nn + 1);
-                MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, nn, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats));
+                MUX_TRY(mux_canon_impl(ctx, W, wtype, (int32_t)N, nn, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st,
+                                       stats));
                 // the canonical assignment has the same (optimal) total
-                finalize_ssp_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
-                    static_cast<const int32_t*>(W), ldw, nn, colr, col_out_dev);
+                finalize_ssp_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
+                    static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, colr, col_out_dev);
                 MUX_CUDA_TRY(cudaGetLastError());
                 MUX_CUDA_TRY(cudaStreamSynchronize(st));
                 if (stats) stats->launches += 4;

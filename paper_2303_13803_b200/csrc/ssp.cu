@@ -83,9 +83,11 @@ struct Cnt {
 };
 
 struct Lvl {
-    const int32_t* A;   // [m][lda] benefits
+    const int32_t* A;   // [nreal][lda] benefits; rows >= nreal are zero (the reference's square padding)
     int64_t lda;
     int32_t m;
+    int32_t nreal;
+    const int32_t* zrow;   // m zeros
     int64_t* p;         // [m] column prices
     int32_t* cor;       // [m] column of row (-1 free)
     int32_t* roc;       // [m] row of column (-1 free)
@@ -108,6 +110,10 @@ struct Lvl {
     int32_t* xscol;     // scanned columns of the current search
     int32_t* xgap;      // global fallback: horizon gaps
 };
+
+__device__ __forceinline__ const int32_t* rowp(const Lvl& L, int32_t i) {
+    return i < L.nreal ? L.A + (int64_t)i * L.lda : L.zrow;
+}
 
 __device__ __forceinline__ int64_t ldv64(const int64_t* p) { return *reinterpret_cast<const volatile int64_t*>(p); }
 __device__ __forceinline__ int32_t ldv32(const int32_t* p) { return *reinterpret_cast<const volatile int32_t*>(p); }
@@ -198,7 +204,7 @@ __device__ __forceinline__ void warp_top32(int32_t m, F keyf, uint64_t& mine, ui
 // Rebuild row i's candidate record: its KC best columns by value a_ij - p_j
 // and tau_i >= the value of every other column (prices only rise afterwards).
 __device__ void refresh_row(const Lvl& L, int32_t i) {
-    const int32_t* Ar = L.A + (int64_t)i * L.lda;
+    const int32_t* Ar = rowp(L, i);
     uint64_t mine, bound;
     // plain L2 loads (pipelined): a price read late is still a price the column
     // had, and prices only rise, so tau stays an upper bound
@@ -303,7 +309,7 @@ __device__ __forceinline__ void release_locks(WTab& T, int32_t nt, const Lvl& L)
 // Dense re-scan of row r at base distance db (= d_r + pi_r): its 32 nearest
 // columns not yet scanned join the search; returns the row's new horizon.
 __device__ int64_t deep_relax(WTab& T, int32_t& nt, const Lvl& L, int32_t r, int64_t db, bool& ok) {
-    const int32_t* Ar = L.A + (int64_t)r * L.lda;
+    const int32_t* Ar = rowp(L, r);
     uint64_t mine, bound;
     warp_top32(L.m, [&](int32_t j) -> uint64_t {
         const int32_t e = hfind(T, j);
@@ -380,7 +386,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
                     if (++deeps > L.deep_budget) { ok = false; break; }
                     const int ee = e0 + src;
                     const int32_t r = T.row[ee];
-                    const int64_t pir = (int64_t)__ldg(L.A + (int64_t)r * L.lda + T.col[ee]) - T.snap[ee];
+                    const int64_t pir = (int64_t)__ldg(rowp(L, r) + T.col[ee]) - T.snap[ee];
                     const int64_t h = deep_relax(T, nt, L, r, T.dist[ee] + pir, ok);
                     if (lane == 0) T.hor[ee] = h;
                     __syncwarp();
@@ -424,7 +430,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
         }
         if (own < 0) { jf = cc; ef = e; D = dmin; result = kDone; break; }
         if (++steps > L.step_budget) { result = kTooBig; break; }
-        const int64_t pir = (int64_t)__ldg(L.A + (int64_t)own * L.lda + cc) - pnow;
+        const int64_t pir = (int64_t)__ldg(rowp(L, own) + cc) - pnow;
         if (lane == 0) { T.st[e] |= kScanned; T.row[e] = own; }
         __syncwarp();
         const int32_t c2 = __ldcg(L.cj + (int64_t)own * KC + lane);
@@ -555,7 +561,7 @@ __device__ __forceinline__ bool x_relax(XTab& X, const Lvl& L, int32_t c, int64_
 // nearer than `thr` joins the search; the row's new horizon is thr.  Callers
 // double the row's reach on each re-scan, so a row is re-scanned O(log) times.
 __device__ int64_t x_deep(XTab& X, const Lvl& L, int32_t r, int64_t db, int64_t thr, bool& ok) {
-    const int32_t* Ar = L.A + (int64_t)r * L.lda;
+    const int32_t* Ar = rowp(L, r);
     constexpr int U = 8;
     for (int32_t j0 = 0; j0 < L.m && ok; j0 += 32 * U) {
         int64_t nd[U];
@@ -647,7 +653,7 @@ __global__ void __launch_bounds__(32, 1) ssp_exclusive_kernel(Lvl L, int32_t nde
                         bal &= bal - 1;
                         const int32_t r = __ldcg(L.roc + col);
                         const int64_t dc = X.dist[col];
-                        const int64_t pir = (int64_t)__ldg(L.A + (int64_t)r * L.lda + col) - __ldcg(L.p + col);
+                        const int64_t pir = (int64_t)__ldg(rowp(L, r) + col) - __ldcg(L.p + col);
                         int64_t hn = x_deep(X, L, r, dc + pir, dmin >= kInf ? kInf : dmin + (dmin - dc > 0 ? dmin - dc : 1), ok);
                         if (lane == 0) X.gap[col] = hn >= kInf ? INT32_MAX : clamp_gap(hn - dc);
                         if (hn < kInf) hn = dc + (int64_t)X.gap[col];   // the stored (possibly saturated) bound
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(32, 1) ssp_exclusive_kernel(Lvl L, int32_t nde
             const int32_t own = __ldcg(L.roc + cc);
             if (own < 0) { jf = cc; D = dmin; break; }
             ++steps;
-            const int64_t pir = (int64_t)__ldg(L.A + (int64_t)own * L.lda + cc) - __ldcg(L.p + cc);
+            const int64_t pir = (int64_t)__ldg(rowp(L, own) + cc) - __ldcg(L.p + cc);
             const int32_t c2 = __ldcg(L.cj + (int64_t)own * KC + lane);
             ok = x_relax(X, L, c2, c2 >= 0 ? dmin + pir + __ldcg(L.p + c2) - __ldcg(L.ca + (int64_t)own * KC + lane) : 0, own);
             const int64_t tg = pir - __ldcg(L.tau + own);
@@ -757,7 +763,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
     unsigned long long steps = 0;
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = L.A + (int64_t)s * L.lda;
+        const int32_t* As = rowp(L, s);
         uint64_t vmin = kNoKey;   // max value as the min of (2^39 - value)
 #pragma unroll
         for (int u = 0; u < DCOLS; ++u) {
@@ -794,7 +800,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
             if (fl[jm] & 2) { jf = jm; D = dmin; break; }
             const int32_t i = rocs[jm];
             if ((jm & (DTHREADS - 1)) == tid) fl[jm] |= 1;   // only the column's owner thread reads its flag
-            const int32_t* Ai = L.A + (int64_t)i * L.lda;
+            const int32_t* Ai = rowp(L, i);
             // the whole row slice and a_i,jm in one batch of loads
             int32_t av[DCOLS];
 #pragma unroll
@@ -857,82 +863,124 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
 
 constexpr int CL = 8;
 constexpr int CTHREADS = 1024;
-constexpr int CCOLS = 2;            // local columns per thread: m <= CL * CTHREADS * CCOLS
+constexpr int CCOLS = 8;            // local columns per thread: m <= CL * CTHREADS * CCOLS = 65536
+constexpr int CBYTES = 25;          // shared bytes per local column: d, p (int64), pred, owner (int32), flag
 
-__device__ __forceinline__ uint64_t cluster_min64(uint64_t v, uint64_t (*slots)[32], uint64_t* bc, int& par,
-                                                  cg::cluster_group& cluster) {
+struct CShared {
+    uint64_t slots[2][32];   // per-warp minima, double-buffered by step parity
+    uint64_t bkey[2];        // cluster-wide minimum
+    int32_t bown[2];         // its column's owner row (-1 = free column)
+    int64_t bprice[2];       // its column's price
+};
+
+// Cluster-wide minimum key.  With `fetch`, warp 0 also reads the winning
+// column's owner row and price from the CTA that holds it (DSMEM) before the
+// CTA barrier, so every thread gets them without another round trip.
+__device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, int& par, cg::cluster_group& cluster,
+                                                      int32_t mc, int32_t* rocs, int64_t* ps, bool fetch,
+                                                      int32_t& own, int64_t& pw) {
     v = wmin64(v);
     const int w = threadIdx.x >> 5;
-    if (lane_id() == 0) slots[par][w] = v;
+    if (lane_id() == 0) S.slots[par][w] = v;
     cluster.sync();
     if (w == 0) {
         uint64_t x = kNoKey;
 #pragma unroll
         for (int r = 0; r < CL; ++r) {
-            const uint64_t* rs = cluster.map_shared_rank(&slots[par][0], r);
+            const uint64_t* rs = cluster.map_shared_rank(&S.slots[par][0], r);
             const uint64_t y = rs[lane_id()];
             x = y < x ? y : x;
         }
         x = wmin64(x);
-        if (lane_id() == 0) bc[par] = x;
+        if (lane_id() == 0) {
+            S.bkey[par] = x;
+            if (fetch && x != kNoKey) {
+                const int32_t j = (int32_t)(x & 0x7FFFFFu);
+                const int owner = j / mc;
+                S.bown[par] = cluster.map_shared_rank(rocs, owner)[j - owner * mc];
+                S.bprice[par] = cluster.map_shared_rank(ps, owner)[j - owner * mc];
+            }
+        }
     }
     __syncthreads();
-    const uint64_t r = bc[par];
+    const uint64_t r = S.bkey[par];
+    if (fetch) { own = S.bown[par]; pw = S.bprice[par]; }
     par ^= 1;
     return r;
 }
 
+// REPL: prices and owners of all m columns replicated in every CTA (12 m
+// bytes; no per-step fetch).  Otherwise each CTA keeps only its slice and the
+// winner's owner / price are fetched from its CTA during the reduction.
+template <bool REPL, int CC>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint64_t slots[2][32];
-    __shared__ uint64_t bc[2];
+    __shared__ CShared S;
     cg::cluster_group cluster = cg::this_cluster();
     const int32_t m = L.m;
     const int32_t mc = (m + CL - 1) / CL;
     const int rank = (int)cluster.block_rank();
     const int32_t c0 = rank * mc;
     const int32_t nloc = max(0, min(mc, m - c0));
-    int64_t* ps = reinterpret_cast<int64_t*>(smem);            // [m] replica
-    int64_t* d = ps + m;                                       // [mc] local
-    int16_t* rocs = reinterpret_cast<int16_t*>(d + mc);        // [m] replica
-    int16_t* pred = rocs + m;                                  // [mc] local
-    uint8_t* fl = reinterpret_cast<uint8_t*>(pred + mc);       // [mc] local: bit0 scanned
+    // REPL: psr[m], rocr[m] replicas first; local slice views ps / rocs point into them
+    int64_t* psr = reinterpret_cast<int64_t*>(smem);
+    int32_t* rocr = reinterpret_cast<int32_t*>(psr + (REPL ? m : 0));
+    int64_t* d = reinterpret_cast<int64_t*>(rocr + (REPL ? ((m + 1) & ~1) : 0));   // [mc] local columns
+    int64_t* ps = REPL ? psr + c0 : d + mc;
+    int32_t* pred = reinterpret_cast<int32_t*>(d + mc + (REPL ? 0 : mc));
+    int32_t* rocs = REPL ? rocr + c0 : pred + mc;
+    uint8_t* fl = reinterpret_cast<uint8_t*>(pred + mc + (REPL ? 0 : mc));       // bit0 scanned
     const int tid = threadIdx.x;
     int par = 0;
     unsigned long long steps = 0;
+    int32_t dummy_own;
+    int64_t dummy_p;
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = L.A + (int64_t)s * L.lda;
-        for (int32_t j = tid; j < m; j += CTHREADS) {
-            ps[j] = __ldcg(L.p + j);
-            rocs[j] = (int16_t)__ldcg(L.roc + j);
+        const int32_t* As = rowp(L, s);
+        if (REPL) {
+            for (int32_t j = tid; j < m; j += CTHREADS) {
+                psr[j] = __ldcg(L.p + j);
+                rocr[j] = __ldcg(L.roc + j);
+            }
+            __syncthreads();
         }
-        __syncthreads();
         uint64_t vmin = kNoKey;
 #pragma unroll
-        for (int u = 0; u < CCOLS; ++u) {
+        for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * CTHREADS;
             if (jj < nloc) {
-                const uint64_t k = (uint64_t)(kDistLim - ((int64_t)__ldg(As + c0 + jj) - ps[c0 + jj]));
+                int64_t pj;
+                if (REPL) {
+                    pj = ps[jj];
+                } else {
+                    pj = __ldcg(L.p + c0 + jj);
+                    ps[jj] = pj;
+                    rocs[jj] = __ldcg(L.roc + c0 + jj);
+                }
+                fl[jj] = 0;
+                const uint64_t k = (uint64_t)(kDistLim - ((int64_t)__ldg(As + c0 + jj) - pj));
                 vmin = k < vmin ? k : vmin;
             }
         }
-        const int64_t pis = kDistLim - (int64_t)cluster_min64(vmin, slots, bc, par, cluster);
+        const int64_t pis = kDistLim - (int64_t)cluster_min_fetch(vmin, S, par, cluster, mc, rocs, ps, false,
+                                                                    dummy_own, dummy_p);
         uint64_t best = kNoKey;
 #pragma unroll
-        for (int u = 0; u < CCOLS; ++u) {
+        for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * CTHREADS;
             if (jj < nloc) {
-                const int32_t j = c0 + jj;
-                const int64_t nd = pis + ps[j] - (int64_t)__ldg(As + j);
+                const int64_t nd = pis + ps[jj] - (int64_t)__ldg(As + c0 + jj);
                 d[jj] = nd;
-                pred[jj] = (int16_t)s;
-                fl[jj] = 0;
-                const uint64_t k = ((uint64_t)nd << 24) | (rocs[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                pred[jj] = s;
+                const uint64_t k = ((uint64_t)nd << 24) | (rocs[jj] < 0 ? 0u : (1u << 23)) | (uint32_t)(c0 + jj);
                 best = k < best ? k : best;
             }
         }
-        best = cluster_min64(best, slots, bc, par, cluster);
+        int32_t i;
+        int64_t pjm;
+        best = cluster_min_fetch(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+        if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
@@ -940,53 +988,51 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
         while (true) {
             const int32_t jm = (int32_t)(best & 0x7FFFFFu);
             const int64_t dmin = (int64_t)(best >> 24);
-            const int32_t i = rocs[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
             // coarse levels: a search past the pop limit is abandoned (row stays free)
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             if (jm >= c0 && jm < c0 + nloc && ((jm - c0) & (CTHREADS - 1)) == tid) fl[jm - c0] |= 1;
-            const int32_t* Ai = L.A + (int64_t)i * L.lda;
-            int32_t av[CCOLS];
+            const int32_t* Ai = rowp(L, i);
+            int32_t av[CC];
 #pragma unroll
-            for (int u = 0; u < CCOLS; ++u) {
+            for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * CTHREADS;
                 av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
             }
-            const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - ps[jm];
+            const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - pjm;
             best = kNoKey;
 #pragma unroll
-            for (int u = 0; u < CCOLS; ++u) {
+            for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * CTHREADS;
                 if (jj < nloc && !(fl[jj] & 1)) {
-                    const int32_t j = c0 + jj;
                     int64_t dj = d[jj];
-                    const int64_t nd = base + ps[j] - (int64_t)av[u];
-                    if (nd < dj) { dj = nd; d[jj] = nd; pred[jj] = (int16_t)i; }
-                    const uint64_t k = ((uint64_t)dj << 24) | (rocs[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                    const int64_t nd = base + ps[jj] - (int64_t)av[u];
+                    if (nd < dj) { dj = nd; d[jj] = nd; pred[jj] = i; }
+                    const uint64_t k = ((uint64_t)dj << 24) | (rocs[jj] < 0 ? 0u : (1u << 23)) | (uint32_t)(c0 + jj);
                     best = k < best ? k : best;
                 }
             }
-            best = cluster_min64(best, slots, bc, par, cluster);
+            best = cluster_min_fetch(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+            if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
             ++steps;
         }
         if (abandon) { cluster.sync(); continue; }
         // dual update on the local scanned columns
 #pragma unroll
-        for (int u = 0; u < CCOLS; ++u) {
+        for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * CTHREADS;
-            if (jj < nloc && (fl[jj] & 1)) L.p[c0 + jj] = ps[c0 + jj] + (D - d[jj]);
+            if (jj < nloc && (fl[jj] & 1)) L.p[c0 + jj] = ps[jj] + (D - d[jj]);
         }
         // the path: predecessors live in their owners' shared memory
         if (rank == 0 && tid == 0) {
             int32_t j = jf;
             while (true) {
                 const int owner = j / mc;
-                const int16_t* pr = cluster.map_shared_rank(pred, owner);
-                const int32_t i = pr[j - owner * mc];
-                const int32_t jn = (i == s) ? -1 : __ldcg(L.cor + i);
-                L.roc[j] = i;
-                L.cor[i] = j;
-                if (i == s) break;
+                const int32_t ii = cluster.map_shared_rank(pred, owner)[j - owner * mc];
+                const int32_t jn = (ii == s) ? -1 : __ldcg(L.cor + ii);
+                L.roc[j] = ii;
+                L.cor[ii] = j;
+                if (ii == s) break;
                 j = jn;
             }
         }
@@ -1000,21 +1046,26 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
 // level setup kernels
 // ---------------------------------------------------------------------------
 
-// A_l[r][c] = W[rows[r]][cols[c]]
-__global__ void gather_kernel(const int32_t* W, int64_t ldw, const int32_t* rows, const int32_t* cols, int32_t m,
-                              int32_t* out) {
+// A_l[r][c] = W[rows[r]][cols[c]] (rows >= N are the zero padding rows)
+__global__ void gather_kernel(const int32_t* W, int64_t ldw, int32_t N, const int32_t* rows, const int32_t* cols,
+                              int32_t m, int32_t* out) {
     for (int32_t r = blockIdx.x; r < m; r += gridDim.x) {
-        const int32_t* Wr = W + (int64_t)rows[r] * ldw;
+        const int32_t ri = rows[r];
+        if (ri >= N) {
+            for (int32_t c = threadIdx.x; c < m; c += blockDim.x) out[(int64_t)r * m + c] = 0;
+            continue;
+        }
+        const int32_t* Wr = W + (int64_t)ri * ldw;
         for (int32_t c = threadIdx.x; c < m; c += blockDim.x) out[(int64_t)r * m + c] = __ldg(Wr + cols[c]);
     }
 }
 
-// base level: p_j = max_i a_ij
-__global__ void colmax_kernel(const int32_t* A, int64_t lda, int32_t m, int64_t* p) {
+// base level: p_j = max_i a_ij (rows >= nreal are zero)
+__global__ void colmax_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
-    int64_t b = INT64_MIN;
-    for (int32_t i = 0; i < m; ++i) {
+    int64_t b = nreal < m ? 0 : INT64_MIN;
+    for (int32_t i = 0; i < nreal && i < m; ++i) {
         const int64_t v = A[(int64_t)i * lda + j];
         b = v > b ? v : b;
     }
@@ -1045,8 +1096,8 @@ __global__ void profit_kernel(const int32_t* A, int64_t lda, int32_t m, const in
 // c-transform: p_j = max_k (A[sub[k]][j] - pi_k) over the coarse rows k.
 // blockIdx.y takes one chunk of the coarse rows; partial maxima meet in an
 // atomicMax (p pre-filled with INT64_MIN).
-__global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t m, const int32_t* sub, const int64_t* pi,
-                                  int32_t mc, int32_t chunk, int64_t* p) {
+__global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t nreal, const int32_t* zrow, int32_t m,
+                                  const int32_t* sub, const int64_t* pi, int32_t mc, int32_t chunk, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     const int32_t k0 = blockIdx.y * chunk, k1 = min(mc, k0 + chunk);
@@ -1055,12 +1106,18 @@ __global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t m, cons
     for (; k + 4 <= k1; k += 4) {
         int64_t v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = (int64_t)__ldg(A + (int64_t)__ldg(sub + k + u) * lda + j) - __ldg(pi + k + u);
+        for (int u = 0; u < 4; ++u) {
+            const int32_t r = __ldg(sub + k + u);
+            const int32_t* Ar = r < nreal ? A + (int64_t)r * lda : zrow;
+            v[u] = (int64_t)__ldg(Ar + j) - __ldg(pi + k + u);
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) b = v[u] > b ? v[u] : b;
     }
     for (; k < k1; ++k) {
-        const int64_t v = (int64_t)__ldg(A + (int64_t)__ldg(sub + k) * lda + j) - __ldg(pi + k);
+        const int32_t r = __ldg(sub + k);
+        const int32_t* Ar = r < nreal ? A + (int64_t)r * lda : zrow;
+        const int64_t v = (int64_t)__ldg(Ar + j) - __ldg(pi + k);
         b = v > b ? v : b;
     }
     if (b != INT64_MIN) atomicMax(reinterpret_cast<long long*>(p + j), (long long)b);
@@ -1100,17 +1157,18 @@ __global__ void finish_kernel(const int32_t* W, int64_t ldw, int32_t n, const in
 // dense certificate (tests / MUX_SSP_CHECK): bad[0] unmatched rows, bad[1]
 // row/column inconsistency, bad[2] dual violations pi_i + p_j < a_ij,
 // bad[3] = first violating (i << 32 | j)
-__global__ void check_kernel(const int32_t* A, int64_t lda, int32_t m, const int32_t* cor, const int32_t* roc,
-                             const int64_t* p, unsigned long long* bad) {
+__global__ void check_kernel(const int32_t* A, int64_t lda, int32_t nreal, const int32_t* zrow, int32_t m,
+                             const int32_t* cor, const int32_t* roc, const int64_t* p, unsigned long long* bad) {
     const int32_t i = blockIdx.x;
     if (i >= m) return;
+    const int32_t* Ai = i < nreal ? A + (int64_t)i * lda : zrow;
     const int32_t j0 = cor[i];
     if (j0 < 0) { if (threadIdx.x == 0) atomicAdd(bad, 1ull); return; }
     if (threadIdx.x == 0 && roc[j0] != i) atomicAdd(bad + 1, 1ull);
-    const int64_t pi = (int64_t)A[(int64_t)i * lda + j0] - p[j0];
+    const int64_t pi = (int64_t)Ai[j0] - p[j0];
     unsigned long long b = 0;
     for (int32_t j = threadIdx.x; j < m; j += blockDim.x)
-        if ((int64_t)A[(int64_t)i * lda + j] - p[j] > pi) {
+        if ((int64_t)Ai[j] - p[j] > pi) {
             ++b;
             atomicCAS(bad + 3, 0ull, ((unsigned long long)i << 32) | (unsigned)j);
         }
@@ -1118,10 +1176,10 @@ __global__ void check_kernel(const int32_t* A, int64_t lda, int32_t m, const int
 }
 
 // row / column sums: generic ordering keys when the caller has none
-__global__ void rowsum_kernel(const int32_t* W, int64_t ldw, int32_t n, double* rs, double* cs) {
+__global__ void rowsum_kernel(const int32_t* W, int64_t ldw, int32_t M, double* rs, double* cs) {
     const int32_t i = blockIdx.x;
     double s = 0;
-    for (int32_t j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int32_t j = threadIdx.x; j < M; j += blockDim.x) {
         const double v = (double)W[(int64_t)i * ldw + j];
         s += v;
         atomicAdd(cs + j, v);
@@ -1141,10 +1199,14 @@ static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 // Multilevel exact solve of the square int32 problem W [n][ldw].
 // rowkey / colkey: host ordering keys (may be null: row / column sums).
 // price_out (device int64 [n], optional): optimal column prices (max form).
-int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const double* rowkey,
+// Solves the reference's square problem of size n = M: rows N..M-1 are the
+// zero padding rows (N <= M).
+int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
                  int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st) {
-    if (n <= 0) { if (total_q) *total_q = 0; return MUX_OK; }
+    const int32_t n = M;
+    if (n <= 0 || N <= 0) { if (total_q) *total_q = 0; return MUX_OK; }
+    if (N > M) { set_error("ssp: needs N <= M"); return MUX_EINVAL; }
     if (n >= (1 << 23)) { set_error("ssp: problem too large"); return MUX_EINVAL; }
     const bool verbose = getenv("MUX_VERBOSE") != nullptr;
     const int fct = std::max(2, atoi(getenv("MUX_SSP_F") ? getenv("MUX_SSP_F") : "2"));
@@ -1159,17 +1221,18 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     auto t0 = std::chrono::steady_clock::now();
 
     // ordering keys -> sorted index lists
-    std::vector<double> rk(n), ck(n);
+    // padding rows sort first (key -inf): the stratified levels keep their share
+    std::vector<double> rk(n, -1e300), ck(n);
     if (rowkey && colkey) {
-        std::copy(rowkey, rowkey + n, rk.begin());
-        std::copy(colkey, colkey + n, ck.begin());
+        std::copy(rowkey, rowkey + N, rk.begin());
+        std::copy(colkey, colkey + M, ck.begin());
     } else {
         MUX_TRY(ctx->ssp.ensure(16ull * n + 256));
         double* d = ctx->ssp.as<double>();
         MUX_CUDA_TRY(cudaMemsetAsync(d, 0, 16ull * n, st));
-        rowsum_kernel<<<n, 256, 0, st>>>(W, ldw, n, d, d + n);
-        MUX_CUDA_TRY(cudaMemcpyAsync(rk.data(), d, 8ull * n, cudaMemcpyDeviceToHost, st));
-        MUX_CUDA_TRY(cudaMemcpyAsync(ck.data(), d + n, 8ull * n, cudaMemcpyDeviceToHost, st));
+        rowsum_kernel<<<N, 256, 0, st>>>(W, ldw, M, d, d + n);
+        MUX_CUDA_TRY(cudaMemcpyAsync(rk.data(), d, 8ull * N, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(ck.data(), d + n, 8ull * M, cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));
     }
     std::vector<int32_t> ro(n), co(n);
@@ -1208,6 +1271,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     auto take = [&](size_t b) { size_t o = off; off += al256(b); return o; };
     const size_t o_cnt = take(sizeof(Cnt));
     const size_t o_tot = take(32);
+    const size_t o_zero = take(4ull * n + 64);
     std::vector<size_t> o_A(nl), o_p(nl), o_cor(nl), o_roc(nl), o_lock(nl), o_cj(nl), o_ca(nl), o_tau(nl), o_in(nl),
         o_re(nl), o_de(nl), o_tr(nl), o_pi(nl), o_sub(nl), o_rows(nl), o_cols(nl);
     for (int l = 0; l < nl; ++l) {
@@ -1227,13 +1291,15 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     Cnt* cnt = reinterpret_cast<Cnt*>(B + o_cnt);
     MUX_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(Cnt), st));
     MUX_CUDA_TRY(cudaMemsetAsync(B + o_tot, 0, 8, st));
+    MUX_CUDA_TRY(cudaMemsetAsync(B + o_zero, 0, 4ull * n + 64, st));
+    const int32_t* zrow = reinterpret_cast<const int32_t*>(B + o_zero);
 
     // upload index lists and gather the coarse matrices
     for (int l = 1; l < nl; ++l) {
         MUX_CUDA_TRY(cudaMemcpyAsync(B + o_rows[l], lv[l].rows.data(), 4ull * lv[l].m, cudaMemcpyHostToDevice, st));
         MUX_CUDA_TRY(cudaMemcpyAsync(B + o_cols[l], lv[l].cols.data(), 4ull * lv[l].m, cudaMemcpyHostToDevice, st));
         gather_kernel<<<std::min<int32_t>(lv[l].m, 4096), 256, 0, st>>>(
-            W, ldw, reinterpret_cast<int32_t*>(B + o_rows[l]), reinterpret_cast<int32_t*>(B + o_cols[l]), lv[l].m,
+            W, ldw, N, reinterpret_cast<int32_t*>(B + o_rows[l]), reinterpret_cast<int32_t*>(B + o_cols[l]), lv[l].m,
             reinterpret_cast<int32_t*>(B + o_A[l]));
     }
     for (int l = 0; l + 1 < nl; ++l)
@@ -1248,7 +1314,9 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_parallel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_exclusive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     const bool use_cluster = !(getenv("MUX_SSP_CLUSTER") && *getenv("MUX_SSP_CLUSTER") == '0');
     int per_sm = 0;
     MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssp_parallel_kernel, PWARPS * 32, psmem));
@@ -1268,6 +1336,8 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         L.A = l ? reinterpret_cast<const int32_t*>(B + o_A[l]) : W;
         L.lda = l ? m : ldw;
         L.m = m;
+        L.nreal = l ? m : N;
+        L.zrow = zrow;
         L.p = reinterpret_cast<int64_t*>(B + o_p[l]);
         L.cor = reinterpret_cast<int32_t*>(B + o_cor[l]);
         L.roc = reinterpret_cast<int32_t*>(B + o_roc[l]);
@@ -1294,7 +1364,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         init_level_kernel<<<g1, 256, 0, st>>>(m, L.cor, L.roc, L.lock, L.tries, in0, stride);
         // prices
         if (l == nl - 1) {
-            colmax_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, m, L.p);
+            colmax_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, L.nreal, m, L.p);
         } else {
             const int32_t mc = lv[l + 1].m;
             int64_t* pic = reinterpret_cast<int64_t*>(B + o_pi[l + 1]);
@@ -1305,7 +1375,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             const int32_t ksplit = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * 8 / g1, mc / 64));
             const int32_t chunk = (mc + ksplit - 1) / ksplit;
             ctransform_kernel<<<dim3(g1, (unsigned)((mc + chunk - 1) / chunk)), 256, 0, st>>>(
-                L.A, L.lda, m, reinterpret_cast<int32_t*>(B + o_sub[l]), pic, mc, chunk, L.p);
+                L.A, L.lda, L.nreal, L.zrow, m, reinterpret_cast<int32_t*>(B + o_sub[l]), pic, mc, chunk, L.p);
             launches += 3;
         }
         cand_kernel<<<(unsigned)std::min<int64_t>(((int64_t)m * 32 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(L);
@@ -1355,10 +1425,18 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
             L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
             const size_t dense_bytes = 21ull * m + 64;
             const int32_t mcl = (m + CL - 1) / CL;
-            const size_t cl_bytes = 10ull * m + 11ull * mcl + 64;
-            if (use_cluster && m <= CL * CTHREADS * CCOLS && m < 32768 && cl_bytes <= xs_budget - 1024) {
-                // long searches: dense Dijkstra over a cluster of CL SMs
-                ssp_cluster_kernel<<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, l == 0 ? 0 : coarse_pops);
+            const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
+            const size_t clr_bytes = 12ull * m + 8 + 13ull * mcl + 64;
+            const int32_t pl = l == 0 ? 0 : coarse_pops;
+            if (use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048) {
+                // long searches: dense Dijkstra over a cluster of CL SMs, replicated prices
+                ssp_cluster_kernel<true, 2><<<CL, CTHREADS, clr_bytes, st>>>(L, ndef_total, pl);
+            } else if (use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048) {
+                // large m: column-sharded cluster tables
+                if (m <= CL * CTHREADS * 4)
+                    ssp_cluster_kernel<false, 4><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
+                else
+                    ssp_cluster_kernel<false, CCOLS><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
             } else if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
                 // long searches: dense Dijkstra on one CTA, tables in shared memory
                 ssp_dense_kernel<<<1, DTHREADS, dense_bytes, st>>>(L, ndef_total);
@@ -1392,7 +1470,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
         if (check && (l == 0 || coarse_exact)) {
             unsigned long long* bad = reinterpret_cast<unsigned long long*>(B + o_tot);
             MUX_CUDA_TRY(cudaMemsetAsync(bad, 0, 32, st));
-            check_kernel<<<m, 256, 0, st>>>(L.A, L.lda, m, L.cor, L.roc, L.p, bad);
+            check_kernel<<<m, 256, 0, st>>>(L.A, L.lda, L.nreal, L.zrow, m, L.cor, L.roc, L.p, bad);
             unsigned long long hb[4] = {0, 0, 0, 0};
             MUX_CUDA_TRY(cudaMemcpyAsync(hb, bad, 32, cudaMemcpyDeviceToHost, st));
             MUX_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1415,7 +1493,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     const int32_t* cor0 = reinterpret_cast<int32_t*>(B + o_cor[0]);
     unsigned long long* tot = reinterpret_cast<unsigned long long*>(B + o_tot);
     MUX_CUDA_TRY(cudaMemsetAsync(tot, 0, 8, st));
-    finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W, ldw, n, cor0, col_out, tot);
+    finish_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(W, ldw, N, cor0, col_out, tot);
     ++launches;
     if (price_out) MUX_CUDA_TRY(cudaMemcpyAsync(price_out, B + o_p[0], 8ull * n, cudaMemcpyDeviceToDevice, st));
     if (cor_out) MUX_CUDA_TRY(cudaMemcpyAsync(cor_out, B + o_cor[0], 4ull * n, cudaMemcpyDeviceToDevice, st));
@@ -1426,7 +1504,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t n, const
     if (total_q) *total_q = (int64_t)ht;
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (stats) {
-        stats->n_rows = n; stats->n_cols = n; stats->n_square = n;
+        stats->n_rows = N; stats->n_cols = M; stats->n_square = n;
         stats->phases = nl;
         stats->rounds = 0;
         stats->bids = (int64_t)(hc.steps + hc.xsteps);

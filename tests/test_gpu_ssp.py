@@ -165,3 +165,45 @@ def test_stats_reported(cuda):
     assert st["levels"] >= 3
     assert st["par_steps"] > 0
     assert st["ms_parallel"] > 0
+
+
+# ------------------------------------------------ rectangular rounds (N < M)
+
+@pytest.mark.parametrize("n,m,q,seed", [(1, 5, 20, 0), (50, 64, 20, 1), (300, 900, 20, 2), (999, 1001, 30, 3),
+                                        (700, 2800, 30, 4)])
+def test_rectangular_predictor_rounds_vs_lsa(cuda, certified, n, m, q, seed):
+    """More jobs than online rows: the reference's zero padding rows are implicit
+    (rows N..M-1 read a shared zero row); the dual certificate covers them."""
+    from paper_2303_13803_b200 import default_table, round_arrays
+    from paper_2303_13803_b200.synth import make_cluster
+    from scipy.optimize import linear_sum_assignment
+    t = default_table()
+    cl = make_cluster(n, m, seed=seed)
+    W = predictor_ref.predict_pairs_exact(t.axes, t.values, cl.x, cl.share, cl.y)
+    Q = np.rint(np.where(W >= 1e-6, W, 0.0) * 2.0 ** q).astype(np.int64)
+    r, c = linear_sum_assignment(Q.astype(np.float64), maximize=True)
+    col, total, st = round_arrays(t, cl.x, cl.share, cl.y, qbits=q, stats=True)
+    assert total == int(Q[r, c].sum())
+    _check_assignment(Q, col, total)
+    assert st["n_square"] == m
+
+
+@pytest.mark.parametrize("n,m,hi,seed", [(100, 400, 1000, 0), (333, 500, 3, 1), (64, 1000, 1 << 20, 2)])
+def test_rectangular_random_vs_lsa(cuda, certified, n, m, hi, seed):
+    Q = np.random.default_rng(seed).integers(0, hi, size=(n, m)).astype(np.int64)
+    col, total = _match(Q)
+    assert total == _lsa(Q)
+    _check_assignment(Q, col, total)
+
+
+def test_rectangular_sharded_cluster_tables(cuda, certified, monkeypatch):
+    """m above the replicated-table limit (16,384 columns) uses column-sharded
+    cluster tables with per-step DSMEM fetches of the winner's owner and price."""
+    from paper_2303_13803_b200 import default_table, round_arrays
+    from paper_2303_13803_b200.synth import make_cluster
+    t = default_table()
+    cl = make_cluster(1200, 20000, seed=5)
+    col, total, st = round_arrays(t, cl.x, cl.share, cl.y, qbits=20, stats=True)
+    monkeypatch.setenv("MUX_SOLVER", "auction")
+    _, t_auc = round_arrays(t, cl.x, cl.share, cl.y, qbits=20)
+    assert total == t_auc

@@ -1,0 +1,6 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+(timeout 300 python tools/ssp_stress.py; N=3000 R=20 timeout 300 python tools/ssp_stress.py) > gpurun_out/stress.log 2>&1
+MUX_VERBOSE=1 timeout 900 python tools/rect_check.py > gpurun_out/rect_check.log 2> gpurun_out/rect_check.err
+timeout 300 python bench.py --steps 4 --warmup 2 --no-cpu --no-e2e --no-mlp > gpurun_out/bench_sq.json 2>/dev/null
+echo finished
