@@ -1335,6 +1335,35 @@ __global__ void finalize_kernel(const void* W, int64_t ldw, int32_t N, int32_t M
     if ((threadIdx.x & 31) == 0 && q) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt->total_q), (unsigned long long)q);
 }
 
+// out[c][r] = in[r][c] (in: rows x cols, 32 x 32 tiles through shared memory)
+__global__ void transpose_i32_kernel(const int32_t* in, int64_t ldi, int32_t rows, int32_t cols, int32_t* out,
+                                     int64_t ldo) {
+    __shared__ int32_t tile[32][33];
+    const int32_t r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int32_t r = r0 + k, c = c0 + threadIdx.x;
+        tile[k][threadIdx.x] = (r < rows && c < cols) ? in[(int64_t)r * ldi + c] : 0;
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int32_t c = c0 + k, r = r0 + threadIdx.x;
+        if (c < cols && r < rows) out[(int64_t)c * ldo + r] = tile[threadIdx.x][k];
+    }
+}
+
+// transposed solve (jobs as rows, n = N) -> original orientation
+__global__ void untranspose_duals_kernel(const int32_t* WT, int64_t ldt, int32_t mreal, int32_t n, const int64_t* pT,
+                                         const int32_t* corT, const int32_t* rocT, int64_t sc, int32_t* col,
+                                         int64_t* price, int32_t* owner) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    col[k] = rocT[k];          // online row k -> its job (or a padding column >= M)
+    const int32_t u = corT[k]; // job / padding column k -> its online row
+    owner[k] = u;
+    const int64_t a = (k < mreal && u >= 0) ? (int64_t)WT[(int64_t)k * ldt + u] : 0;
+    price[k] = (u >= 0 ? a - pT[u] : 0) * sc;
+}
+
 __global__ void finalize_ssp_kernel(const int32_t* W, int64_t ldw, int32_t N, int32_t M, const int32_t* col,
                                     int32_t* out) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1395,6 +1424,46 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         // N < M: the zero padding rows of the reference's square problem are
         // implicit; N > M (more online rows than jobs) stays on the auction
         const bool rect_ok = !(getenv("MUX_SSP_RECT") && *getenv("MUX_SSP_RECT") == '0');
+        const bool use_ssp_t = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && M >= 1 && N >= 2 &&
+                               N > M && rect_ok;
+        if (use_ssp_t) {
+            // N > M: solve the transposed M x N problem (jobs as rows, the padding
+            // columns of the reference become implicit zero rows), then map the
+            // assignment and the duals back for the canonicalisation
+            const int32_t nn = (int32_t)N, mm = (int32_t)M;
+            const int64_t ldt = ((int64_t)nn + 3) / 4 * 4;
+            size_t off = 0;
+            auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
+            const size_t o_wt = take(4ull * mm * ldt), o_pt = take(8ull * nn), o_ct = take(4ull * nn),
+                         o_rt = take(4ull * nn), o_co = take(4ull * nn), o_pr = take(8ull * nn), o_ow = take(4ull * nn);
+            MUX_TRY(ctx->auc.ensure(off));
+            char* base = ctx->auc.as<char>();
+            int32_t* WT = reinterpret_cast<int32_t*>(base + o_wt);
+            int64_t* pT = reinterpret_cast<int64_t*>(base + o_pt);
+            int32_t* corT = reinterpret_cast<int32_t*>(base + o_ct);
+            int32_t* rocT = reinterpret_cast<int32_t*>(base + o_rt);
+            int32_t* colr = reinterpret_cast<int32_t*>(base + o_co);
+            int64_t* price = reinterpret_cast<int64_t*>(base + o_pr);
+            int32_t* owner = reinterpret_cast<int32_t*>(base + o_ow);
+            transpose_i32_kernel<<<dim3((unsigned)((nn + 31) / 32), (unsigned)((mm + 31) / 32)), dim3(32, 8), 0, st>>>(
+                static_cast<const int32_t*>(W), ldw, nn, mm, WT, ldt);
+            int64_t tq = 0;
+            MUX_TRY(mux_ssp_impl(ctx, WT, ldt, mm, nn, colkey, rowkey, col_out_dev, &tq, pT, corT, rocT, stats, st));
+            // original orientation: col_of_row[u] = rocT[u]; owner of job v = corT[v];
+            // column (job) prices = the transposed rows' profits
+            untranspose_duals_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(WT, ldt, mm, nn, pT, corT, rocT,
+                                                                                 (int64_t)nn + 1, colr, price, owner);
+            const char* cs = getenv("MUX_CANON");
+            if (!(cs && *cs == '0'))
+                MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, mm, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats));
+            finalize_ssp_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
+                static_cast<const int32_t*>(W), ldw, nn, mm, colr, col_out_dev);
+            MUX_CUDA_TRY(cudaGetLastError());
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            if (stats) { stats->launches += 4; stats->n_rows = N; stats->n_cols = M; stats->total_q = tq; }
+            if (total_q) *total_q = tq;
+            return MUX_OK;
+        }
         const bool use_ssp = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && N >= 1 && M >= 2 &&
                              (N == M || (N < M && rect_ok));
         if (use_ssp) {

@@ -207,3 +207,28 @@ def test_rectangular_sharded_cluster_tables(cuda, certified, monkeypatch):
     monkeypatch.setenv("MUX_SOLVER", "auction")
     _, t_auc = round_arrays(t, cl.x, cl.share, cl.y, qbits=20)
     assert total == t_auc
+
+
+@pytest.mark.parametrize("n,m,q,seed", [(5, 1, 20, 0), (64, 50, 20, 1), (900, 300, 20, 2), (1001, 999, 30, 3),
+                                        (2800, 700, 30, 4)])
+def test_more_rows_than_jobs_vs_lsa(cuda, certified, n, m, q, seed):
+    """N > M: the transposed problem (jobs as rows) is solved and the assignment
+    and duals are mapped back; the canonicalisation runs in the original orientation."""
+    from paper_2303_13803_b200 import default_table, round_arrays
+    from paper_2303_13803_b200.synth import make_cluster
+    from scipy.optimize import linear_sum_assignment
+    t = default_table()
+    cl = make_cluster(n, m, seed=seed)
+    W = predictor_ref.predict_pairs_exact(t.axes, t.values, cl.x, cl.share, cl.y)
+    Q = np.rint(np.where(W >= 1e-6, W, 0.0) * 2.0 ** q).astype(np.int64)
+    r, c = linear_sum_assignment(Q.astype(np.float64), maximize=True)
+    col, total = round_arrays(t, cl.x, cl.share, cl.y, qbits=q)
+    assert total == int(Q[r, c].sum())
+    _check_assignment(Q, col, total)
+
+
+def test_more_rows_than_jobs_random(cuda, certified):
+    Q = np.random.default_rng(9).integers(0, 1000, size=(600, 250)).astype(np.int64)
+    col, total = _match(Q)
+    assert total == _lsa(Q)
+    _check_assignment(Q, col, total)

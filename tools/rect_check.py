@@ -12,7 +12,7 @@ from paper_2303_13803_b200.synth import make_cluster
 from oracle import predictor_ref as pr
 t = default_table()
 fails = 0
-for n, m, q, seed in [(50, 64, 20, 0), (300, 900, 20, 1), (1000, 3000, 30, 2), (999, 1001, 30, 3), (1500, 6000, 20, 4)]:
+for n, m, q, seed in [(50, 64, 20, 0), (300, 900, 20, 1), (1000, 3000, 30, 2), (999, 1001, 30, 3), (1500, 6000, 20, 4), (64, 50, 20, 5), (3000, 1000, 30, 6), (1001, 999, 20, 7)]:
     cl = make_cluster(n, m, seed=seed)
     W = pr.predict_pairs_exact(pr.DEFAULT_AXES, pr.default_table_values(), cl.x, cl.share, cl.y)
     Q = np.rint(np.where(W >= 1e-6, W, 0) * 2.0 ** q).astype(np.int64)
@@ -24,7 +24,7 @@ for n, m, q, seed in [(50, 64, 20, 0), (300, 900, 20, 1), (1000, 3000, 30, 2), (
     fails += not ok
     print(f"{n}x{m} q={q}: {tot} want {want} {'OK' if ok else 'FAIL'} ({1e3*(time.time()-t0):.1f} ms, match {st['ms_match']:.1f})", flush=True)
 os.environ["MUX_SSP_CHECK"] = "0"
-for n, m, q, want in [(4000, 12000, 20, 2413913397), (10000, 40000, 20, 6111445217), (10000, 40000, 30, None)]:
+for n, m, q, want in [(4000, 12000, 20, 2413913397), (12000, 4000, 20, 3042374446), (10000, 40000, 20, 6111445217), (10000, 40000, 30, None)]:
     cl = make_cluster(n, m, seed=0)
     for rep in range(2):
         t0 = time.time()
