@@ -80,6 +80,8 @@ struct Cnt {
     uint32_t errors;
     unsigned long long steps, deep, aborts, augs, xsteps, xdeep, refresh, overflow;
     long long xcyc[4];   // exclusive kernel: pop, horizon re-scans, scan steps, augment
+    int32_t xq, xretry;   // concurrent cluster searches: next deferred row, rows to retry
+    unsigned long long xaborts;
 };
 
 struct Lvl {
@@ -871,11 +873,13 @@ struct CShared {
     uint64_t bkey[2];        // cluster-wide minimum
     int32_t bown[2];         // its column's owner row (-1 = free column)
     int64_t bprice[2];       // its column's price
+    int32_t qnext;           // concurrent mode: the deferred row this cluster takes next
 };
 
 // Cluster-wide minimum key.  With `fetch`, warp 0 also reads the winning
 // column's owner row and price from the CTA that holds it (DSMEM) before the
 // CTA barrier, so every thread gets them without another round trip.
+template <int CLS>
 __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, int& par, cg::cluster_group& cluster,
                                                       int32_t mc, int32_t* rocs, int64_t* ps, bool fetch,
                                                       int32_t& own, int64_t& pw) {
@@ -886,7 +890,7 @@ __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, in
     if (w == 0) {
         uint64_t x = kNoKey;
 #pragma unroll
-        for (int r = 0; r < CL; ++r) {
+        for (int r = 0; r < CLS; ++r) {
             const uint64_t* rs = cluster.map_shared_rank(&S.slots[par][0], r);
             const uint64_t y = rs[lane_id()];
             x = y < x ? y : x;
@@ -912,13 +916,13 @@ __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, in
 // REPL: prices and owners of all m columns replicated in every CTA (12 m
 // bytes; no per-step fetch).  Otherwise each CTA keeps only its slice and the
 // winner's owner / price are fetched from its CTA during the reduction.
-template <bool REPL, int CC>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
+template <bool REPL, int CC, int CLS>
+__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t conc) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CShared S;
     cg::cluster_group cluster = cg::this_cluster();
     const int32_t m = L.m;
-    const int32_t mc = (m + CL - 1) / CL;
+    const int32_t mc = (m + CLS - 1) / CLS;
     const int rank = (int)cluster.block_rank();
     const int32_t c0 = rank * mc;
     const int32_t nloc = max(0, min(mc, m - c0));
@@ -935,7 +939,19 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
     unsigned long long steps = 0;
     int32_t dummy_own;
     int64_t dummy_p;
-    for (int32_t q = 0; q < ndef; ++q) {
+    // conc: several clusters take deferred rows from a shared counter; every
+    // popped column is locked (non-blocking CAS) and the tree is validated
+    // against the global state only at augment time, under the locks
+    const int32_t lid = (1 << 30) | (int32_t)(blockIdx.x / CLS);
+    for (int32_t qq = 0;; ++qq) {
+        int32_t q = qq;
+        if (conc) {
+            if (rank == 0 && tid == 0) S.qnext = atomicAdd(&L.cnt->xq, 1);
+            cluster.sync();
+            q = *cluster.map_shared_rank(&S.qnext, 0);
+            cluster.sync();
+        }
+        if (q >= ndef) break;
         const int32_t s = L.defer[q];
         const int32_t* As = rowp(L, s);
         if (REPL) {
@@ -945,6 +961,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
             }
             __syncthreads();
         }
+        // one reduction finds both the source's profit (the largest a_sj - p_j)
+        // and the first pop (that column, at distance 0; free columns first)
         uint64_t vmin = kNoKey;
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
@@ -959,39 +977,48 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
                     rocs[jj] = __ldcg(L.roc + c0 + jj);
                 }
                 fl[jj] = 0;
-                const uint64_t k = (uint64_t)(kDistLim - ((int64_t)__ldg(As + c0 + jj) - pj));
+                const int64_t v = pj - (int64_t)__ldg(As + c0 + jj);   // = -(a_sj - p_j)
+                const uint64_t k = ((uint64_t)(v + kDistLim) << 24) | ((REPL ? rocs[jj] : __ldcg(L.roc + c0 + jj)) < 0 ? 0u : (1u << 23)) |
+                                   (uint32_t)(c0 + jj);
                 vmin = k < vmin ? k : vmin;
-            }
-        }
-        const int64_t pis = kDistLim - (int64_t)cluster_min_fetch(vmin, S, par, cluster, mc, rocs, ps, false,
-                                                                    dummy_own, dummy_p);
-        uint64_t best = kNoKey;
-#pragma unroll
-        for (int u = 0; u < CC; ++u) {
-            const int32_t jj = tid + u * CTHREADS;
-            if (jj < nloc) {
-                const int64_t nd = pis + ps[jj] - (int64_t)__ldg(As + c0 + jj);
-                d[jj] = nd;
-                pred[jj] = s;
-                const uint64_t k = ((uint64_t)nd << 24) | (rocs[jj] < 0 ? 0u : (1u << 23)) | (uint32_t)(c0 + jj);
-                best = k < best ? k : best;
             }
         }
         int32_t i;
         int64_t pjm;
-        best = cluster_min_fetch(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+        const uint64_t k0 = cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+        const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
+        uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * CTHREADS;
+            if (jj < nloc) {
+                d[jj] = pis + ps[jj] - (int64_t)__ldg(As + c0 + jj);
+                pred[jj] = s;
+            }
+        }
         if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
         bool abandon = false;
+        int32_t pend_jj = -1, pend_old = 0;   // conc: the last CAS, recorded after the next reduction
         while (true) {
             const int32_t jm = (int32_t)(best & 0x7FFFFFu);
             const int64_t dmin = (int64_t)(best >> 24);
-            if (i < 0) { jf = jm; D = dmin; break; }
+            if (pend_jj >= 0) { fl[pend_jj] |= pend_old == 0 ? 4 : 8; pend_jj = -1; }
+            const bool own_jm = jm >= c0 && jm < c0 + nloc && ((jm - c0) & (CTHREADS - 1)) == tid;
+            if (i < 0) {
+                jf = jm;
+                D = dmin;
+                if (conc && own_jm) fl[jm - c0] |= atomicCAS(L.lock + jm, 0, lid) == 0 ? 4 : 8;
+                break;
+            }
             // coarse levels: a search past the pop limit is abandoned (row stays free)
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (jm >= c0 && jm < c0 + nloc && ((jm - c0) & (CTHREADS - 1)) == tid) fl[jm - c0] |= 1;
+            if (own_jm) {
+                fl[jm - c0] |= 1;
+                if (conc) { pend_old = atomicCAS(L.lock + jm, 0, lid); pend_jj = jm - c0; }
+            }
             const int32_t* Ai = rowp(L, i);
             int32_t av[CC];
 #pragma unroll
@@ -1012,9 +1039,37 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
                     best = k < best ? k : best;
                 }
             }
-            best = cluster_min_fetch(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+            best = cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
             if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
             ++steps;
+        }
+        if (pend_jj >= 0) { fl[pend_jj] |= pend_old == 0 ? 4 : 8; pend_jj = -1; }
+        if (conc) {
+            // validate the tree under the locks: every scanned column (and the free
+            // end) locked by us, with the price and owner this search started from
+            uint64_t okv = 1;
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t jj = tid + u * CTHREADS;
+                if (jj < nloc && ((fl[jj] & 1) || c0 + jj == jf)) {
+                    const uint8_t f = fl[jj];
+                    if (!(f & 4) || __ldcg(L.p + c0 + jj) != ps[jj] || __ldcg(L.roc + c0 + jj) != rocs[jj]) okv = 0;
+                }
+            }
+            const bool valid = cluster_min_fetch<CLS>(okv, S, par, cluster, mc, rocs, ps, false, dummy_own, dummy_p) == 1;
+            if (!valid || abandon) {
+#pragma unroll
+                for (int u = 0; u < CC; ++u) {
+                    const int32_t jj = tid + u * CTHREADS;
+                    if (jj < nloc && (fl[jj] & 4)) atomicExch(L.lock + c0 + jj, 0);
+                }
+                if (!valid && rank == 0 && tid == 0) {
+                    L.retry[atomicAdd(&L.cnt->xretry, 1)] = s;
+                    atomicAdd(&L.cnt->xaborts, 1ull);
+                }
+                cluster.sync();
+                continue;
+            }
         }
         if (abandon) { cluster.sync(); continue; }
         // dual update on the local scanned columns
@@ -1038,6 +1093,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cl
         }
         __threadfence();
         cluster.sync();
+        if (conc) {
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t jj = tid + u * CTHREADS;
+                if (jj < nloc && (fl[jj] & 4)) atomicExch(L.lock + c0 + jj, 0);
+            }
+        }
     }
     if (rank == 0 && tid == 0) atomicAdd(&L.cnt->xsteps, steps);
 }
@@ -1314,9 +1376,15 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_parallel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_exclusive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    const int cl_size = getenv("MUX_SSP_CL") ? atoi(getenv("MUX_SSP_CL")) : CL;
+    // clusters running long searches concurrently (1 = one at a time)
+    const int32_t conc_clusters = getenv("MUX_SSP_CONC") ? atoi(getenv("MUX_SSP_CONC")) : 4;
     const bool use_cluster = !(getenv("MUX_SSP_CLUSTER") && *getenv("MUX_SSP_CLUSTER") == '0');
     int per_sm = 0;
     MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssp_parallel_kernel, PWARPS * 32, psmem));
@@ -1428,15 +1496,41 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
             const size_t clr_bytes = 12ull * m + 8 + 13ull * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
-            if (use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048) {
-                // long searches: dense Dijkstra over a cluster of CL SMs, replicated prices
-                ssp_cluster_kernel<true, 2><<<CL, CTHREADS, clr_bytes, st>>>(L, ndef_total, pl);
-            } else if (use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048) {
-                // large m: column-sharded cluster tables
-                if (m <= CL * CTHREADS * 4)
-                    ssp_cluster_kernel<false, 4><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
-                else
-                    ssp_cluster_kernel<false, CCOLS><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
+            const bool repl_ok = use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048;
+            const bool shard_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
+            auto launch_cl = [&](int32_t nrows, int32_t conc, int32_t nclusters) {
+                const unsigned g = (unsigned)(CL * nclusters);
+                if (repl_ok) {
+                    if (cl_size == 16 && !conc)
+                        ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0);
+                    else if (cl_size == 4 && !conc)
+                        ssp_cluster_kernel<true, 4, 4><<<4, CTHREADS, 12ull * m + 8 + 13ull * ((m + 3) / 4) + 64, st>>>(L, nrows, pl, 0);
+                    else
+                        ssp_cluster_kernel<true, 2, CL><<<g, CTHREADS, clr_bytes, st>>>(L, nrows, pl, conc);
+                } else if (m <= CL * CTHREADS * 4) {
+                    ssp_cluster_kernel<false, 4, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc);
+                } else {
+                    ssp_cluster_kernel<false, CCOLS, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc);
+                }
+            };
+            if (repl_ok || shard_ok) {
+                // several long searches at once on separate clusters (locks + validation),
+                // then whatever conflicted on one cluster alone
+                const int32_t ncl = std::min<int32_t>(conc_clusters, ndef_total);
+                if (ncl >= 2) {
+                    L.retry = bufs[0];
+                    MUX_CUDA_TRY(cudaMemsetAsync(&cnt->xq, 0, 2 * sizeof(int32_t), st));
+                    launch_cl(ndef_total, 1, ncl);
+                    int32_t nre = 0;
+                    MUX_CUDA_TRY(cudaMemcpyAsync(&nre, &cnt->xretry, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+                    if (nre > 0) {
+                        L.defer = bufs[0];
+                        launch_cl(nre, 0, 1);
+                    }
+                } else {
+                    launch_cl(ndef_total, 0, 1);
+                }
             } else if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
                 // long searches: dense Dijkstra on one CTA, tables in shared memory
                 ssp_dense_kernel<<<1, DTHREADS, dense_bytes, st>>>(L, ndef_total);
