@@ -1384,7 +1384,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     const int cl_size = getenv("MUX_SSP_CL") ? atoi(getenv("MUX_SSP_CL")) : CL;
     // clusters running long searches concurrently (1 = one at a time)
-    const int32_t conc_clusters = getenv("MUX_SSP_CONC") ? atoi(getenv("MUX_SSP_CONC")) : 4;
+    const int32_t conc_clusters = getenv("MUX_SSP_CONC") ? atoi(getenv("MUX_SSP_CONC")) : 1;
     const bool use_cluster = !(getenv("MUX_SSP_CLUSTER") && *getenv("MUX_SSP_CLUSTER") == '0');
     int per_sm = 0;
     MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssp_parallel_kernel, PWARPS * 32, psmem));
