@@ -165,6 +165,15 @@ def cpu_reference(n_target, m_target, seed, budget_s=20.0):
     return est_s * 1e3, sample, t_match + per_pair * npairs
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of ssp_cluster_kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01b", "ncu_cluster_traffic.json")) as f:
+            return json.load(f)["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -319,11 +328,12 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, peak_kind = peaks()
-    # dominant kernel: ssp_dense_kernel (csrc/ssp.cu), the single-CTA Dijkstra
-    # that runs the long augmenting paths of every level.  Algorithmic bytes =
-    # one weight row (4*m_level) per pop (SURVEY §8d's per-row-read unit),
-    # summed over its pops; time = its CUDA-event duration on the launching
-    # stream inside the solve.
+    # dominant kernel: ssp_cluster_kernel (csrc/ssp.cu), the thread-block-cluster
+    # Dijkstra that runs the long augmenting paths of every level.  Algorithmic
+    # bytes = one weight row (4*m_level) per pop (SURVEY §8d's per-row-read
+    # unit), summed over its pops; time = its CUDA-event duration on the
+    # launching stream inside the solve.  `traffic`: DRAM bytes per launch from
+    # the committed ncu --set full capture of the same kernel (profiles/).
     dense_ms = sum(x["ms_dense"] for x in stats_all) / len(stats_all)
     dense_bytes = sum(x["dense_bytes"] for x in stats_all) / len(stats_all)
     achieved = dense_bytes / (dense_ms / 1e3) / 1e9 if dense_ms > 0 else 0.0
@@ -342,14 +352,16 @@ def run_ours(args, rank, world, local_rank):
                    "n_online": n, "n_offline": m, "qbits": q, "parallelism": f"replicas x{world}",
                    "l2": "flushed (256 MB write) between timed steps; W (400 MB) > L2"},
         "pair_scores_per_s": n * m * world / (t_step / 1e3),
-        "roofline": {"bound": "hbm", "kernel": "ssp_dense_kernel", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "ssp_cluster_kernel", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None, "algorithmic_bytes": dense_bytes, "kernel_ms": dense_ms,
+                     "traffic": ncu_traffic(), "traffic_note": "DRAM read+write bytes per launch (ncu, profiles/r01b)",
+                     "algorithmic_bytes": dense_bytes, "kernel_ms": dense_ms,
+                     "algorithmic_bytes_per_launch": dense_bytes / max(1.0, sum(x["dense_launches"] for x in stats_all) / len(stats_all)),
                      "note": "latency-bound: one dependent pop per step (sequential Dijkstra); bytes = 4*m per pop",
                      "share_of_step": dense_ms / t_step},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": int(s["launches"]) + 3,
-        "solver": {k: s[k] for k in ("levels", "par_steps", "dense_steps", "dense_searches", "ms_dense", "ms_parallel",
+        "solver": {k: s[k] for k in ("levels", "par_steps", "dense_steps", "dense_searches", "dense_launches", "ms_dense", "ms_parallel",
                                      "row_scans", "total_q", "ms_match", "ms_canon", "canon_searches", "tight_edges",
                                      "dual_sweeps")},
         "ms_match": auc_ms, "ms_per_step_all": times,

@@ -107,6 +107,7 @@ typedef struct {
     double  ms_dense;        /* device time of the dense kernel (events)    */
     double  ms_parallel;     /* device time of the parallel passes (events) */
     double  dense_bytes;     /* weight-row bytes the dense kernel read (4 m per pop) */
+    int64_t dense_launches;  /* launches of the long-path kernel              */
 } mux_stats_t;
 
 typedef struct mux_ctx mux_ctx_t;

@@ -43,7 +43,8 @@ class MuxStats(ctypes.Structure):
                 ("tight_edges", ctypes.c_int64), ("dual_sweeps", ctypes.c_int64),
                 ("levels", ctypes.c_int64), ("par_steps", ctypes.c_int64), ("dense_steps", ctypes.c_int64),
                 ("dense_searches", ctypes.c_int64), ("ms_dense", ctypes.c_double),
-                ("ms_parallel", ctypes.c_double), ("dense_bytes", ctypes.c_double)]
+                ("ms_parallel", ctypes.c_double), ("dense_bytes", ctypes.c_double),
+                ("dense_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

@@ -1394,7 +1394,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     cudaEvent_t ev[4];
     for (auto& e : ev) MUX_CUDA_TRY(cudaEventCreate(&e));
     double ms_dense = 0, ms_par = 0, dense_bytes = 0;
-    int64_t dense_searches = 0;
+    int64_t dense_searches = 0, dense_launches = 0;
     unsigned long long xsteps_prev = 0;
     double ms_levels[64] = {0};
     for (int l = nl - 1; l >= 0; --l) {
@@ -1556,6 +1556,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             dense_bytes += 4.0 * (double)m * (double)(hc.xsteps - xsteps_prev);
             xsteps_prev = hc.xsteps;
             dense_searches += ndef_total;
+            dense_launches += ndef_total > 0 ? 1 : 0;
         }
         if (hc.errors) {
             set_error(std::string("ssp: device error flags ") + std::to_string(hc.errors));
@@ -1615,6 +1616,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         stats->ms_dense = ms_dense;
         stats->ms_parallel = ms_par;
         stats->dense_bytes = dense_bytes;
+        stats->dense_launches = dense_launches;
     }
     for (auto& e : ev) cudaEventDestroy(e);
     if (verbose) fprintf(stderr, "[ssp] n %d levels %d total %.3f ms (host wall), dense %.3f ms, parallel %.3f ms\n", n, nl, ms,

@@ -10,8 +10,8 @@ CMD="python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e --no-mlp"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_10k.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "ncu launches exit $?" >> gpurun_out/ncu_launches.log
 python tools/ssp_one.py > gpurun_out/ssp_one.log 2>&1 && \
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:ssp_dense_kernel -c 10 -o gpurun_out/ssp_dense_10k python tools/ssp_one.py > gpurun_out/ncu_dense.log 2>&1
-echo "ncu dense exit $?" >> gpurun_out/ncu_dense.log
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:ssp_cluster_kernel -c 12 -o gpurun_out/ssp_cluster_10k python tools/ssp_one.py > gpurun_out/ncu_cluster.log 2>&1
+echo "ncu cluster exit $?" >> gpurun_out/ncu_cluster.log
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:ssp_parallel_kernel -c 3 -o gpurun_out/ssp_parallel_10k python tools/ssp_one.py > gpurun_out/ncu_par.log 2>&1
 echo "ncu parallel exit $?" >> gpurun_out/ncu_par.log
 echo finished
