@@ -913,13 +913,90 @@ __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, in
     return r;
 }
 
+// Push mode (REPL kernels): no cluster barrier per step.  Lanes 0..CLS-1 of
+// every warp write the warp's minimum straight into slot [rank*32 + warp] of
+// CTA `lane` with st.async, which completes bytes on that CTA's mbarrier; warp
+// 0 of each CTA waits for all CLS*32 minima (one-way DSMEM latency instead of
+// barrier.cluster's all-to-all round trip, its release fence and its L1
+// invalidate), reduces them and re-arms the mbarrier for the buffer's next
+// use.  Buffers alternate by step parity: a CTA can only push step k+2 into a
+// buffer after receiving every CTA's step k+1, which each CTA sends only after
+// it has consumed step k from that buffer.
+template <int CLS>
+struct CPush {
+    uint64_t slots[2][CLS * 32];
+    uint64_t bar[2];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int CLS>
+__device__ __forceinline__ void cpush_init(CPush<CLS>& P) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t a = smem_u32(&P.bar[b]);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t a = smem_u32(&P.bar[b]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(CLS * 32 * 8) : "memory");
+        }
+    }
+}
+
+template <int CLS>
+__device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPush<CLS>& P, int& par, uint32_t& ph, int rank) {
+    v = wmin64(v);
+    const int w = threadIdx.x >> 5, ln = lane_id();
+    const uint32_t lb = smem_u32(&P.bar[par]);
+    if (ln < CLS) {
+        const uint32_t la = smem_u32(&P.slots[par][rank * 32 + w]);
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(ln));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(ln));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"(v), "r"(rb)
+                     : "memory");
+    }
+    if (w == 0) {
+        const uint32_t parity = (ph >> par) & 1u;
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(lb), "r"(parity)
+                : "memory");
+        }
+        uint64_t x = kNoKey;
+#pragma unroll
+        for (int r = 0; r < CLS; ++r) {
+            const uint64_t y = P.slots[par][r * 32 + ln];
+            x = y < x ? y : x;
+        }
+        x = wmin64(x);
+        if (ln == 0) {
+            S.bkey[par] = x;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * 32 * 8) : "memory");
+        }
+    }
+    ph ^= 1u << par;
+    __syncthreads();
+    const uint64_t r = S.bkey[par];
+    par ^= 1;
+    return r;
+}
+
 // REPL: prices and owners of all m columns replicated in every CTA (12 m
 // bytes; no per-step fetch).  Otherwise each CTA keeps only its slice and the
 // winner's owner / price are fetched from its CTA during the reduction.
 template <bool REPL, int CC, int CLS>
-__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t conc) {
+__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t conc, int32_t push) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CShared S;
+    __shared__ __align__(16) CPush<REPL ? CLS : 1> P;
     cg::cluster_group cluster = cg::this_cluster();
     const int32_t m = L.m;
     const int32_t mc = (m + CLS - 1) / CLS;
@@ -939,6 +1016,11 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
     unsigned long long steps = 0;
     int32_t dummy_own;
     int64_t dummy_p;
+    uint32_t ph = 0;
+    if (REPL && push) {
+        cpush_init(P);
+        cluster.sync();
+    }
     // conc: several clusters take deferred rows from a shared counter; every
     // popped column is locked (non-blocking CAS) and the tree is validated
     // against the global state only at augment time, under the locks
@@ -985,7 +1067,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
         }
         int32_t i;
         int64_t pjm;
-        const uint64_t k0 = cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+        const uint64_t k0 = (REPL && push) ? cluster_min_push<CLS>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+                                           : cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
         const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
         uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
 #pragma unroll
@@ -1039,7 +1122,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
                     best = k < best ? k : best;
                 }
             }
-            best = cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+            best = (REPL && push) ? cluster_min_push<CLS>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+                                  : cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
             if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
             ++steps;
         }
@@ -1376,9 +1460,13 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_parallel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_exclusive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    // REPL kernels carry the push-exchange buffers (2 * CLS * 32 * 8 B) in static shared memory
+    const size_t push_b8 = sizeof(CPush<CL>), push_b4 = sizeof(CPush<4>), push_b16 = sizeof(CPush<16>);
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b4)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b16)));
+    // per-step exchange of the long-path kernel: st.async + mbarrier push (default) or cluster barrier
+    const int32_t cpush = !(getenv("MUX_SSP_PUSH") && *getenv("MUX_SSP_PUSH") == '0');
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
@@ -1496,21 +1584,21 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
             const size_t clr_bytes = 12ull * m + 8 + 13ull * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
-            const bool repl_ok = use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048;
+            const bool repl_ok = use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048 - push_b8;
             const bool shard_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
             auto launch_cl = [&](int32_t nrows, int32_t conc, int32_t nclusters) {
                 const unsigned g = (unsigned)(CL * nclusters);
                 if (repl_ok) {
-                    if (cl_size == 16 && !conc)
-                        ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0);
+                    if (cl_size == 16 && !conc && 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64 <= xs_budget - 2048 - push_b16)
+                        ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0, cpush);
                     else if (cl_size == 4 && !conc)
-                        ssp_cluster_kernel<true, 4, 4><<<4, CTHREADS, 12ull * m + 8 + 13ull * ((m + 3) / 4) + 64, st>>>(L, nrows, pl, 0);
+                        ssp_cluster_kernel<true, 4, 4><<<4, CTHREADS, 12ull * m + 8 + 13ull * ((m + 3) / 4) + 64, st>>>(L, nrows, pl, 0, cpush);
                     else
-                        ssp_cluster_kernel<true, 2, CL><<<g, CTHREADS, clr_bytes, st>>>(L, nrows, pl, conc);
+                        ssp_cluster_kernel<true, 2, CL><<<g, CTHREADS, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
                 } else if (m <= CL * CTHREADS * 4) {
-                    ssp_cluster_kernel<false, 4, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc);
+                    ssp_cluster_kernel<false, 4, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc, cpush);
                 } else {
-                    ssp_cluster_kernel<false, CCOLS, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc);
+                    ssp_cluster_kernel<false, CCOLS, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc, cpush);
                 }
             };
             if (repl_ok || shard_ok) {
