@@ -121,13 +121,14 @@ __device__ __forceinline__ int64_t ldv64(const int64_t* p) { return *reinterpret
 __device__ __forceinline__ int32_t ldv32(const int32_t* p) { return *reinterpret_cast<const volatile int32_t*>(p); }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// 64-bit warp minimum as two 32-bit redux.sync reductions (high word, then
+// the low word among the lanes holding the minimal high word): two dependent
+// REDUX ops instead of five shuffle pairs on the search's critical path.
 __device__ __forceinline__ uint64_t wmin64(uint64_t v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
-        v = w < v ? w : v;
-    }
-    return v;
+    const uint32_t hi = (uint32_t)(v >> 32), lo = (uint32_t)v;
+    const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+    const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+    return ((uint64_t)mh << 32) | ml;
 }
 __device__ __forceinline__ int64_t wmax64s(int64_t v) {
 #pragma unroll
@@ -930,7 +931,7 @@ struct CPush {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-template <int CLS>
+template <int CLS, int NW>
 __device__ __forceinline__ void cpush_init(CPush<CLS>& P) {
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -942,12 +943,12 @@ __device__ __forceinline__ void cpush_init(CPush<CLS>& P) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
             const uint32_t a = smem_u32(&P.bar[b]);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(CLS * 32 * 8) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(CLS * NW * 8) : "memory");
         }
     }
 }
 
-template <int CLS>
+template <int CLS, int NW>
 __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPush<CLS>& P, int& par, uint32_t& ph, int rank) {
     v = wmin64(v);
     const int w = threadIdx.x >> 5, ln = lane_id();
@@ -973,13 +974,13 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
         uint64_t x = kNoKey;
 #pragma unroll
         for (int r = 0; r < CLS; ++r) {
-            const uint64_t y = P.slots[par][r * 32 + ln];
+            const uint64_t y = ln < NW ? P.slots[par][r * 32 + ln] : kNoKey;
             x = y < x ? y : x;
         }
         x = wmin64(x);
         if (ln == 0) {
             S.bkey[par] = x;
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * 32 * 8) : "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 8) : "memory");
         }
     }
     ph ^= 1u << par;
@@ -992,8 +993,8 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
 // REPL: prices and owners of all m columns replicated in every CTA (12 m
 // bytes; no per-step fetch).  Otherwise each CTA keeps only its slice and the
 // winner's owner / price are fetched from its CTA during the reduction.
-template <bool REPL, int CC, int CLS>
-__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t conc, int32_t push) {
+template <bool REPL, int CC, int CLS, int NT = CTHREADS>
+__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t conc, int32_t push) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CShared S;
     __shared__ __align__(16) CPush<REPL ? CLS : 1> P;
@@ -1017,8 +1018,10 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
     int32_t dummy_own;
     int64_t dummy_p;
     uint32_t ph = 0;
+    if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;   // slots of warps beyond NT/32
+    __syncthreads();
     if (REPL && push) {
-        cpush_init(P);
+        cpush_init<REPL ? CLS : 1, NT / 32>(P);
         cluster.sync();
     }
     // conc: several clusters take deferred rows from a shared counter; every
@@ -1037,7 +1040,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
         const int32_t s = L.defer[q];
         const int32_t* As = rowp(L, s);
         if (REPL) {
-            for (int32_t j = tid; j < m; j += CTHREADS) {
+            for (int32_t j = tid; j < m; j += NT) {
                 psr[j] = __ldcg(L.p + j);
                 rocr[j] = __ldcg(L.roc + j);
             }
@@ -1048,7 +1051,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
         uint64_t vmin = kNoKey;
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
-            const int32_t jj = tid + u * CTHREADS;
+            const int32_t jj = tid + u * NT;
             if (jj < nloc) {
                 int64_t pj;
                 if (REPL) {
@@ -1067,13 +1070,13 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
         }
         int32_t i;
         int64_t pjm;
-        const uint64_t k0 = (REPL && push) ? cluster_min_push<CLS>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+        const uint64_t k0 = (REPL && push) ? cluster_min_push<CLS, NT / 32>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
                                            : cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
         const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
         uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
-            const int32_t jj = tid + u * CTHREADS;
+            const int32_t jj = tid + u * NT;
             if (jj < nloc) {
                 d[jj] = pis + ps[jj] - (int64_t)__ldg(As + c0 + jj);
                 pred[jj] = s;
@@ -1089,7 +1092,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
             const int32_t jm = (int32_t)(best & 0x7FFFFFu);
             const int64_t dmin = (int64_t)(best >> 24);
             if (pend_jj >= 0) { fl[pend_jj] |= pend_old == 0 ? 4 : 8; pend_jj = -1; }
-            const bool own_jm = jm >= c0 && jm < c0 + nloc && ((jm - c0) & (CTHREADS - 1)) == tid;
+            const bool own_jm = jm >= c0 && jm < c0 + nloc && ((jm - c0) & (NT - 1)) == tid;
             if (i < 0) {
                 jf = jm;
                 D = dmin;
@@ -1106,14 +1109,14 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
             int32_t av[CC];
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const int32_t jj = tid + u * CTHREADS;
+                const int32_t jj = tid + u * NT;
                 av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
             }
             const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - pjm;
             best = kNoKey;
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const int32_t jj = tid + u * CTHREADS;
+                const int32_t jj = tid + u * NT;
                 if (jj < nloc && !(fl[jj] & 1)) {
                     int64_t dj = d[jj];
                     const int64_t nd = base + ps[jj] - (int64_t)av[u];
@@ -1122,7 +1125,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
                     best = k < best ? k : best;
                 }
             }
-            best = (REPL && push) ? cluster_min_push<CLS>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            best = (REPL && push) ? cluster_min_push<CLS, NT / 32>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
                                   : cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
             if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
             ++steps;
@@ -1134,7 +1137,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
             uint64_t okv = 1;
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const int32_t jj = tid + u * CTHREADS;
+                const int32_t jj = tid + u * NT;
                 if (jj < nloc && ((fl[jj] & 1) || c0 + jj == jf)) {
                     const uint8_t f = fl[jj];
                     if (!(f & 4) || __ldcg(L.p + c0 + jj) != ps[jj] || __ldcg(L.roc + c0 + jj) != rocs[jj]) okv = 0;
@@ -1144,7 +1147,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
             if (!valid || abandon) {
 #pragma unroll
                 for (int u = 0; u < CC; ++u) {
-                    const int32_t jj = tid + u * CTHREADS;
+                    const int32_t jj = tid + u * NT;
                     if (jj < nloc && (fl[jj] & 4)) atomicExch(L.lock + c0 + jj, 0);
                 }
                 if (!valid && rank == 0 && tid == 0) {
@@ -1159,7 +1162,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
         // dual update on the local scanned columns
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
-            const int32_t jj = tid + u * CTHREADS;
+            const int32_t jj = tid + u * NT;
             if (jj < nloc && (fl[jj] & 1)) L.p[c0 + jj] = ps[jj] + (D - d[jj]);
         }
         // the path: predecessors live in their owners' shared memory
@@ -1180,7 +1183,7 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1) ssp_c
         if (conc) {
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const int32_t jj = tid + u * CTHREADS;
+                const int32_t jj = tid + u * NT;
                 if (jj < nloc && (fl[jj] & 4)) atomicExch(L.lock + c0 + jj, 0);
             }
         }
@@ -1464,6 +1467,12 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     const size_t push_b8 = sizeof(CPush<CL>), push_b4 = sizeof(CPush<4>), push_b16 = sizeof(CPush<16>);
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b4)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 8, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    // threads per CTA of the replicated long-path cluster kernel: 512 (4 columns per
+    // thread) by default -- fewer warps to reduce and to wait for at each pop's CTA
+    // barrier; 256 / 1024 selectable (all cover m <= 16,384)
+    const int cl_nt = getenv("MUX_SSP_CT") ? atoi(getenv("MUX_SSP_CT")) : 512;
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b16)));
     // per-step exchange of the long-path kernel: st.async + mbarrier push (default) or cluster barrier
     const int32_t cpush = !(getenv("MUX_SSP_PUSH") && *getenv("MUX_SSP_PUSH") == '0');
@@ -1593,6 +1602,10 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
                         ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0, cpush);
                     else if (cl_size == 4 && !conc)
                         ssp_cluster_kernel<true, 4, 4><<<4, CTHREADS, 12ull * m + 8 + 13ull * ((m + 3) / 4) + 64, st>>>(L, nrows, pl, 0, cpush);
+                    else if (cl_nt == 512)
+                        ssp_cluster_kernel<true, 4, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
+                    else if (cl_nt == 256)
+                        ssp_cluster_kernel<true, 8, CL, 256><<<g, 256, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
                     else
                         ssp_cluster_kernel<true, 2, CL><<<g, CTHREADS, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
                 } else if (m <= CL * CTHREADS * 4) {
