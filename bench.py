@@ -167,11 +167,13 @@ def cpu_reference(n_target, m_target, seed, budget_s=20.0):
 
 def ncu_traffic():
     """DRAM bytes per launch of ssp_cluster_kernel from the committed ncu capture."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01b", "ncu_cluster_traffic.json")) as f:
-            return json.load(f)["dram_bytes_per_launch"]
-    except Exception:
-        return None
+    for rnd in ("r01c", "r01b"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "ncu_cluster_traffic.json")) as f:
+                return json.load(f)["dram_bytes_per_launch"], rnd
+        except Exception:
+            continue
+    return None, None
 
 
 def run_reference(args, rank, world):
@@ -338,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
     dense_bytes = sum(x["dense_bytes"] for x in stats_all) / len(stats_all)
     achieved = dense_bytes / (dense_ms / 1e3) / 1e9 if dense_ms > 0 else 0.0
     auc_ms = sum(match_ms) / len(match_ms)
+    traffic, traffic_src = ncu_traffic()
     cpu = None
     if not args.no_cpu:
         cpu_ms, sample, _ = cpu_reference(n, m, args.seed)
@@ -354,7 +357,7 @@ def run_ours(args, rank, world, local_rank):
         "pair_scores_per_s": n * m * world / (t_step / 1e3),
         "roofline": {"bound": "hbm", "kernel": "ssp_cluster_kernel", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": ncu_traffic(), "traffic_note": "DRAM read+write bytes per launch (ncu, profiles/r01b)",
+                     "traffic": traffic, "traffic_note": f"DRAM read+write bytes per launch (ncu --set full, profiles/{traffic_src})",
                      "algorithmic_bytes": dense_bytes, "kernel_ms": dense_ms,
                      "algorithmic_bytes_per_launch": dense_bytes / max(1.0, sum(x["dense_launches"] for x in stats_all) / len(stats_all)),
                      "note": "latency-bound: one dependent pop per step (sequential Dijkstra); bytes = 4*m per pop",

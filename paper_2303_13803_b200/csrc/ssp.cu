@@ -990,6 +990,74 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
     return r;
 }
 
+// Push mode 2: every warp waits on the mbarrier and reduces the CLS*NW
+// minima itself, so a step has no CTA barrier at all.  The mbarrier then
+// counts NW arrivals per phase: each warp arrives (warp 0 with the expected
+// bytes) once it has read the buffer, which arms the buffer's next phase and
+// also certifies that no warp still reads it.
+template <int CLS, int NW>
+__device__ __forceinline__ void cpush_init_all(CPush<CLS>& P) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t a = smem_u32(&P.bar[b]);
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(NW) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (lane_id() == 0) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t a = smem_u32(&P.bar[b]);
+            if (threadIdx.x == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(CLS * NW * 8) : "memory");
+            else
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+        }
+    }
+}
+
+template <int CLS, int NW>
+__device__ __forceinline__ uint64_t cluster_min_push_all(uint64_t v, CPush<CLS>& P, int& par, uint32_t& ph, int rank) {
+    v = wmin64(v);
+    const int w = threadIdx.x >> 5, ln = lane_id();
+    const uint32_t lb = smem_u32(&P.bar[par]);
+    if (ln < CLS) {
+        const uint32_t la = smem_u32(&P.slots[par][rank * 32 + w]);
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(ln));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(ln));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"(v), "r"(rb)
+                     : "memory");
+    }
+    const uint32_t parity = (ph >> par) & 1u;
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(lb), "r"(parity)
+            : "memory");
+    }
+    uint64_t x = kNoKey;
+#pragma unroll
+    for (int r = 0; r < CLS; ++r) {
+        const uint64_t y = ln < NW ? P.slots[par][r * 32 + ln] : kNoKey;
+        x = y < x ? y : x;
+    }
+    x = wmin64(x);   // warp-synchronous: every lane's reads are done past here
+    if (ln == 0) {
+        if (w == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 8) : "memory");
+        else
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lb) : "memory");
+    }
+    ph ^= 1u << par;
+    par ^= 1;
+    return x;
+}
+
 // REPL: prices and owners of all m columns replicated in every CTA (12 m
 // bytes; no per-step fetch).  Otherwise each CTA keeps only its slice and the
 // winner's owner / price are fetched from its CTA during the reduction.
@@ -1021,7 +1089,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
     if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;   // slots of warps beyond NT/32
     __syncthreads();
     if (REPL && push) {
-        cpush_init<REPL ? CLS : 1, NT / 32>(P);
+        if (push == 2) cpush_init_all<REPL ? CLS : 1, NT / 32>(P);
+        else cpush_init<REPL ? CLS : 1, NT / 32>(P);
         cluster.sync();
     }
     // conc: several clusters take deferred rows from a shared counter; every
@@ -1070,7 +1139,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
         }
         int32_t i;
         int64_t pjm;
-        const uint64_t k0 = (REPL && push) ? cluster_min_push<CLS, NT / 32>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+        const uint64_t k0 = (REPL && push == 2) ? cluster_min_push_all<CLS, NT / 32>(vmin, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
                                            : cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
         const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
         uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
@@ -1125,7 +1195,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
                     best = k < best ? k : best;
                 }
             }
-            best = (REPL && push) ? cluster_min_push<CLS, NT / 32>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            best = (REPL && push == 2) ? cluster_min_push_all<CLS, NT / 32>(best, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
                                   : cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
             if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
             ++steps;
@@ -1467,6 +1538,9 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     const size_t push_b8 = sizeof(CPush<CL>), push_b4 = sizeof(CPush<4>), push_b16 = sizeof(CPush<16>);
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b4)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 8, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     // threads per CTA of the replicated long-path cluster kernel: 512 (4 columns per
@@ -1475,7 +1549,8 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     const int cl_nt = getenv("MUX_SSP_CT") ? atoi(getenv("MUX_SSP_CT")) : 512;
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b16)));
     // per-step exchange of the long-path kernel: st.async + mbarrier push (default) or cluster barrier
-    const int32_t cpush = !(getenv("MUX_SSP_PUSH") && *getenv("MUX_SSP_PUSH") == '0');
+    // 0 = cluster barrier, 1 = push + warp-0 reduction + CTA barrier, 2 = push + every warp reduces
+    const int32_t cpush = getenv("MUX_SSP_PUSH") ? atoi(getenv("MUX_SSP_PUSH")) : 1;
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
@@ -1602,6 +1677,12 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
                         ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0, cpush);
                     else if (cl_size == 4 && !conc)
                         ssp_cluster_kernel<true, 4, 4><<<4, CTHREADS, 12ull * m + 8 + 13ull * ((m + 3) / 4) + 64, st>>>(L, nrows, pl, 0, cpush);
+                    else if (cl_nt == 512 && mcl <= 512)
+                        ssp_cluster_kernel<true, 1, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
+                    else if (cl_nt == 512 && mcl <= 1024)
+                        ssp_cluster_kernel<true, 2, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
+                    else if (cl_nt == 512 && mcl <= 1536)
+                        ssp_cluster_kernel<true, 3, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
                     else if (cl_nt == 512)
                         ssp_cluster_kernel<true, 4, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
                     else if (cl_nt == 256)
