@@ -949,7 +949,8 @@ __device__ __forceinline__ void cpush_init(CPush<CLS>& P) {
 }
 
 template <int CLS, int NW>
-__device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPush<CLS>& P, int& par, uint32_t& ph, int rank) {
+__device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPush<CLS>& P, int& par, uint32_t& ph, int rank,
+                                                     uint64_t& cand2) {
     v = wmin64(v);
     const int w = threadIdx.x >> 5, ln = lane_id();
     const uint32_t lb = smem_u32(&P.bar[par]);
@@ -971,13 +972,17 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
                 : "r"(lb), "r"(parity)
                 : "memory");
         }
-        uint64_t x = kNoKey;
+        uint64_t x = kNoKey, x2 = kNoKey;   // this lane's smallest and second smallest of its CLS slots
 #pragma unroll
         for (int r = 0; r < CLS; ++r) {
             const uint64_t y = ln < NW ? P.slots[par][r * 32 + ln] : kNoKey;
-            x = y < x ? y : x;
+            x2 = y < x2 ? y : x2;
+            if (y < x) { x2 = x; x = y; }
         }
+        const uint64_t xl = x;
         x = wmin64(x);
+        // per lane: the best key other than the winner (its warp-min gives the runner-up pop)
+        cand2 = xl == x ? x2 : xl;
         if (ln == 0) {
             S.bkey[par] = x;
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 8) : "memory");
@@ -1086,10 +1091,11 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
     int32_t dummy_own;
     int64_t dummy_p;
     uint32_t ph = 0;
+    uint64_t cand2 = kNoKey;
     if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;   // slots of warps beyond NT/32
     __syncthreads();
     if (REPL && push) {
-        if (push == 2) cpush_init_all<REPL ? CLS : 1, NT / 32>(P);
+        if ((push & 3) == 2) cpush_init_all<REPL ? CLS : 1, NT / 32>(P);
         else cpush_init<REPL ? CLS : 1, NT / 32>(P);
         cluster.sync();
     }
@@ -1139,8 +1145,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
         }
         int32_t i;
         int64_t pjm;
-        const uint64_t k0 = (REPL && push == 2) ? cluster_min_push_all<CLS, NT / 32>(vmin, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
-            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+        const uint64_t k0 = (REPL && (push & 3) == 2) ? cluster_min_push_all<CLS, NT / 32>(vmin, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank, cand2)
                                            : cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
         const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
         uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
@@ -1182,6 +1188,20 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
                 const int32_t jj = tid + u * NT;
                 av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
             }
+            // runner-up prefetch (push mode, bit 4): while this step's row loads are in
+            // flight, warp 0 pulls this CTA's slice of the row owning the runner-up
+            // column into L2 with one bulk prefetch -- it is often the next pop
+            if (REPL && (push & 4) && tid < 32) {
+                const uint64_t k2 = wmin64(cand2);
+                if (k2 != kNoKey && tid == 0) {
+                    const int32_t i2 = rocr[k2 & 0x7FFFFFu];
+                    if (i2 >= 0 && i2 < L.nreal && nloc > 0) {
+                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(L.A + (int64_t)i2 * L.lda + c0) & ~(uintptr_t)15;
+                        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(L.A + (int64_t)i2 * L.lda + c0 + nloc) + 15) & ~(uintptr_t)15;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+                    }
+                }
+            }
             const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - pjm;
             best = kNoKey;
 #pragma unroll
@@ -1195,8 +1215,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
                     best = k < best ? k : best;
                 }
             }
-            best = (REPL && push == 2) ? cluster_min_push_all<CLS, NT / 32>(best, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
-            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            best = (REPL && (push & 3) == 2) ? cluster_min_push_all<CLS, NT / 32>(best, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
+            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank, cand2)
                                   : cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
             if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
             ++steps;
@@ -1550,7 +1570,10 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b16)));
     // per-step exchange of the long-path kernel: st.async + mbarrier push (default) or cluster barrier
     // 0 = cluster barrier, 1 = push + warp-0 reduction + CTA barrier, 2 = push + every warp reduces
-    const int32_t cpush = getenv("MUX_SSP_PUSH") ? atoi(getenv("MUX_SSP_PUSH")) : 1;
+    // | 4 = runner-up row prefetch into L2 (MUX_SSP_PF, push mode 1 only)
+    const int32_t cpush_mode = getenv("MUX_SSP_PUSH") ? atoi(getenv("MUX_SSP_PUSH")) : 1;
+    const bool cpf = cpush_mode == 1 && !(getenv("MUX_SSP_PF") && *getenv("MUX_SSP_PF") == '0');
+    const int32_t cpush = cpush_mode | (cpf ? 4 : 0);
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
