@@ -1192,8 +1192,10 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
             // flight, warp 0 pulls this CTA's slice of the row owning the runner-up
             // column into L2 with one bulk prefetch -- it is often the next pop
             if (REPL && (push & 4) && tid < 32) {
-                const uint64_t k2 = wmin64(cand2);
-                if (k2 != kNoKey && tid == 0) {
+                // bit 8: every lane prefetches its own candidate (the best key of its warp
+                // slot over the CLS CTAs, winner excluded) -- up to NW rows per step
+                const uint64_t k2 = (push & 8) ? cand2 : wmin64(cand2);
+                if (k2 != kNoKey && ((push & 8) || tid == 0)) {
                     const int32_t i2 = rocr[k2 & 0x7FFFFFu];
                     if (i2 >= 0 && i2 < L.nreal && nloc > 0) {
                         const uintptr_t a0 = reinterpret_cast<uintptr_t>(L.A + (int64_t)i2 * L.lda + c0) & ~(uintptr_t)15;
@@ -1572,8 +1574,10 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     // 0 = cluster barrier, 1 = push + warp-0 reduction + CTA barrier, 2 = push + every warp reduces
     // | 4 = runner-up row prefetch into L2 (MUX_SSP_PF, push mode 1 only)
     const int32_t cpush_mode = getenv("MUX_SSP_PUSH") ? atoi(getenv("MUX_SSP_PUSH")) : 1;
-    const bool cpf = cpush_mode == 1 && !(getenv("MUX_SSP_PF") && *getenv("MUX_SSP_PF") == '0');
-    const int32_t cpush = cpush_mode | (cpf ? 4 : 0);
+    // MUX_SSP_PF: 0 off, 1 runner-up row (default), 2 every warp-0 lane's candidate row
+    const int pf_mode = getenv("MUX_SSP_PF") ? atoi(getenv("MUX_SSP_PF")) : 1;
+    const bool cpf = cpush_mode == 1 && pf_mode > 0;
+    const int32_t cpush = cpush_mode | (cpf ? 4 : 0) | (cpf && pf_mode == 2 ? 8 : 0);
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
