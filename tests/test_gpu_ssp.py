@@ -133,6 +133,25 @@ def test_long_path_kernels_agree(cuda, certified, monkeypatch):
         assert total == want, env
 
 
+@pytest.mark.parametrize("env", [
+    {"MUX_SSP_PUSH": "0"},                          # barrier.cluster exchange
+    {"MUX_SSP_PUSH": "1", "MUX_SSP_PF": "0"},       # st.async push, no prefetch
+    {"MUX_SSP_PUSH": "2"},                          # push, every warp reduces
+    {"MUX_SSP_CT": "1024"}, {"MUX_SSP_CT": "256"},  # CTA sizes (default 512)
+    {"MUX_SSP_CL": "16"}, {"MUX_SSP_CL": "4"},      # cluster sizes (default 8)
+    {"MUX_SSP_PF": "2"},
+])
+def test_cluster_exchange_variants(cuda, certified, monkeypatch, env):
+    """Per-pop exchange modes and CTA / cluster shapes of the long-path kernel
+    (csrc/ssp.cu ssp_cluster_kernel) give the same optimum; the dual
+    certificate is checked at every level (MUX_SSP_CHECK=1)."""
+    cl, Q = _pred_Q(2000, 32, 30)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, total = _match(Q, keys=(cl.x, cl.y))
+    assert total == _lsa(Q), env
+
+
 def test_serial_and_parallel_searches_agree(cuda, certified, monkeypatch):
     """Lock-based concurrent warp searches vs one search at a time."""
     cl, Q = _pred_Q(1000, 40, 30)
