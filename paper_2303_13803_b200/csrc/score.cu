@@ -156,18 +156,24 @@ score_exact_kernel(DevTable t, const RowFeat* __restrict__ rf, const ColFeat* __
         if (live[q]) c[q] = cf[col0 + q];
         else { c[q].j0 = 0; c[q].j1 = 0; c[q].wj0 = 0.0; c[q].wj1 = 0.0; }
     }
+    // Table offsets split into a column part (j * nk, fixed per thread) and a
+    // row part (i * nj * nk + k, four per row) so the inner loop does one
+    // 32-bit add per corner; the float64 operation order is unchanged.
+    int32_t cj[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { cj[q][0] = c[q].j0 * nk; cj[q][1] = c[q].j1 * nk; }
+    const int32_t njk = nj * nk;
     const int64_t row_begin = (int64_t)blockIdx.y * kRowsPerCta;
     const int64_t row_end = min(n, row_begin + kRowsPerCta);
     for (int64_t row = row_begin; row < row_end; ++row) {
         const RowFeat r = rf[row];
-        const int32_t ii[2] = {r.i0, r.i1};
+        const int32_t ri[2][2] = {{r.i0 * njk + r.k0, r.i0 * njk + r.k1},
+                                  {r.i1 * njk + r.k0, r.i1 * njk + r.k1}};
         const double wi[2] = {r.wi0, r.wi1};
-        const int32_t kk[2] = {r.k0, r.k1};
         const double wk[2] = {r.wk0, r.wk1};
         double w[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int32_t jj[2] = {c[q].j0, c[q].j1};
             const double wj[2] = {c[q].wj0, c[q].wj1};
             double acc = 0.0;
 #pragma unroll
@@ -175,10 +181,9 @@ score_exact_kernel(DevTable t, const RowFeat* __restrict__ rf, const ColFeat* __
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                     const double wij = __dmul_rn(wi[a], wj[b]);
-                    const double* vrow = V + ((int64_t)ii[a] * nj + jj[b]) * nk;
 #pragma unroll
                     for (int g = 0; g < 2; ++g)
-                        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(wij, wk[g]), vrow[kk[g]]));
+                        acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(wij, wk[g]), V[ri[a][g] + cj[q][b]]));
                 }
             acc = fmin(1.0, fmax(0.0, acc));
             w[q] = live[q] ? acc : 0.0;
