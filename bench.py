@@ -15,17 +15,21 @@ a single-CTA dense Dijkstra for long paths) and the tie canonicalisation
 feature arrays already resident in HBM (device-timed with CUDA events on the
 launching stream); `e2e` is the same round through the C-ABI `mux_round` with
 HOST feature arrays (H2D of features and D2H of col_of_row inside the timed
-region).  With N GPUs each rank solves its own replica (weak scaling, replicas
-only in round 1 -- see DESIGN.md); timing is the max over ranks.
+region).  With N GPUs each rank solves its own snapshot (seed + rank): the
+round does not shard usefully, so `value` stays the per-round
+latency (max over ranks) and replica throughput is reported separately.
+When tests/golden holds the CPU-computed optimal total for the workload
+(scipy LSA on the same integer weights), the round's total must equal it.
 
-`--impl reference` times the CPU oracle port of the reference algorithm
-(oracle/: scalar trilinear predict_point per pair + the O(n^3) Kuhn-Munkres)
-on a bounded sample of the same workload and extrapolates to the metric's
-10k x 10k round (the reference itself takes hours there).
+`--impl reference` runs the unmodified reference package (baseline/_ref,
+pip-installed from /root/reference/pkg) on one host core: measured
+`schedule()` rounds at 64^2 (the timed steps) and 256^2..1024^2, extrapolated
+to the metric's 10k x 10k round (hours of CPU time).
 """
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -121,53 +125,171 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm (oracle port of the reference algorithm)
+# CPU reference arm: the unmodified reference `muxsim` package
 # ---------------------------------------------------------------------------
 
-def cpu_reference(n_target, m_target, seed, budget_s=20.0):
-    """Time the oracle port on a bounded sample; extrapolate to n_target x m_target.
+def load_reference():
+    """Import the reference package unmodified: baseline/_ref (pip-installed
+    from /root/reference/pkg, travels to the GPU box) or, in the build
+    container only, /root/reference/pkg/src.  Returns (modules, path) or None."""
+    import importlib
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if not os.path.isfile(os.path.join(path, "muxsim", "scheduler.py")):
+            continue
+        sys.path.insert(0, path)
+        try:
+            mods = {k: importlib.import_module(f"muxsim.{k}")
+                    for k in ("core", "gpu_state", "scheduler", "simengine", "matching", "predictor")}
+        finally:
+            sys.path.remove(path)
+        if not os.path.abspath(mods["scheduler"].__file__).startswith(os.path.abspath(path)):
+            continue
+        return mods, path
+    return None
 
-    predict: the scalar restatement of predictor.predict_point (the reference's
-    per-pair loop body) timed on a sample of pairs -> per-pair cost x N*M.
-    match:   the C restatement of matching._solve_min_assignment (O(n^3)) on a
-             predictor-derived k x k sample -> cost x (n/k)^3.
-    """
-    from oracle import matching_ref, predictor_ref
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_round_ms(ref, n, m, seed):
+    """Wall time of one reference `schedule()` round (scheduler.py:220-241) on the
+    synthetic snapshot make_cluster(n, m, seed): records built with the
+    reference's own types, default_table(SimConfig()), SchedulerConfig(), now=900."""
+    from paper_2303_13803_b200.synth import make_cluster, records
+
+    class Core:
+        WorkloadProfile = ref["core"].WorkloadProfile
+        OnlineWorkload = ref["core"].OnlineWorkload
+        OfflineWorkload = ref["core"].OfflineWorkload
+        HealthState = ref["gpu_state"].HealthState
+
+    cl = make_cluster(n, m, seed=seed)
+    onl, off, states = records(cl, core=Core)
+    table = ref["simengine"].default_table(ref["simengine"].SimConfig())
+    cfg = ref["scheduler"].SchedulerConfig()
+    t0 = time.perf_counter()
+    asg = ref["scheduler"].schedule(onl, off, states, table, cfg, 900.0)
+    dt = time.perf_counter() - t0
+    return dt * 1e3, asg, (cl, table)
+
+
+def reference_match_ms(ref, cl, table):
+    """Wall time of the reference's public max_weight_matching (matching.py:148-208)
+    alone, on the graph its round builds (weights from its public predict_point)."""
+    mt, pr = ref["matching"], ref["predictor"]
+    L = [f"u{i}" for i in range(cl.n)]
+    R = [f"v{j}" for j in range(cl.m)]
+    w = {}
+    for i in range(cl.n):
+        for j in range(cl.m):
+            x = pr.predict_point(table, float(cl.x[i]), float(cl.y[j]), float(cl.share[i]))
+            if x > 0.0:
+                w[(L[i], R[j])] = x
+    g = mt.BipartiteGraph(tuple(L), tuple(R), w)
+    t0 = time.perf_counter()
+    mt.max_weight_matching(g)
+    return (time.perf_counter() - t0) * 1e3, w
+
+
+def lsa_ms(cl, table_vals_fn):
+    from scipy.optimize import linear_sum_assignment
+    W = table_vals_fn(cl)
+    t0 = time.perf_counter()
+    linear_sum_assignment(W, maximize=True)
+    return (time.perf_counter() - t0) * 1e3
+
+
+def reference_estimate(ref, n, m, seed, k1, k2):
+    """Measured reference rounds at k1^2 and k2^2 (k2 = 2 k1) and the solver
+    alone on both; extrapolated to n x m: predict per pair x N*M plus the
+    Kuhn-Munkres time x (n/k2)^e, e fitted on the k1 -> k2 solves."""
+    rounds, solves = {}, {}
+    for k in (k1 // 2, k1, k2):
+        ms, _asg, (cl, table) = reference_round_ms(ref, k, k, seed)
+        rounds[k] = ms
+        if k >= k1:
+            solves[k], _w = reference_match_ms(ref, cl, table)
+    e = math.log(solves[k2] / solves[k1]) / math.log(k2 / k1)
+    e = min(3.2, max(2.5, e))
+    pred_per_pair = max(0.0, rounds[k2] - solves[k2]) / float(k2 * k2)
+    n_sq = max(n, m)
+    est = pred_per_pair * n * m + solves[k2] * (n_sq / float(k2)) ** e
+    sample = (f"reference muxsim.scheduler.schedule(), 1 core ({cpu_model()}): measured rounds "
+              f"{', '.join(f'{k}^2 {v / 1e3:.2f} s' for k, v in rounds.items())}; solver alone "
+              f"{', '.join(f'{k}^2 {v / 1e3:.2f} s' for k, v in solves.items())} (fit n^{e:.2f}); "
+              f"predict {pred_per_pair * 1e3:.2f} us/pair; EXTRAPOLATED to {n}x{m}")
+    measured = {"round_ms": rounds, "solve_ms": solves, "solve_exponent": e, "predict_us_per_pair": pred_per_pair * 1e3}
+    return est, sample, measured
+
+
+def pin_one_core():
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+    except (AttributeError, OSError):
+        pass
+    return 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own scheduler on this host's cores.
+
+    Rank 0 alone runs (other ranks exit at once).  The reference is
+    single-threaded Python + numpy; it is pinned to one core.  Each timed
+    step is one full `schedule()` round at 64 x 64 (BASELINE config 1),
+    measured.  The 10k x 10k metric is out of reach (~hours), so the
+    line's value is extrapolated from MEASURED rounds at 256^2 / 512^2 /
+    1024^2 split into phases: predict loop (per pair, x N*M) and the
+    Kuhn-Munkres solve (x (n/1024)^e, e fitted on the measured 512 -> 1024
+    solves).  scipy's linear_sum_assignment (C) is timed beside it."""
+    if rank != 0:
+        return
+    got = load_reference()
+    if got is None:
+        print(json.dumps({"impl": "reference", "unavailable": "reference muxsim package not found in baseline/_ref"}))
+        return
+    ref, ref_path = got
+    cores = pin_one_core()
+    small = []
+    for s in range(args.warmup + args.steps):
+        ms, _asg, _ = reference_round_ms(ref, 64, 64, args.seed + s)
+        if s >= args.warmup:
+            small.append(ms)
+    est, sample, measured = reference_estimate(ref, args.n, args.m, args.seed, 512, 1024)
+    # scipy LSA (single-thread C, not the reference) on the same weights
+    from oracle import predictor_ref
     from paper_2303_13803_b200.synth import make_cluster
-    t_axes = predictor_ref.DEFAULT_AXES
     vals = predictor_ref.default_table_values()
-    k = 1024
-    cl = make_cluster(k, k, seed=seed)
-    # predict sample
-    rng = np.random.default_rng(seed)
-    npairs = 0
-    us = rng.integers(0, k, 2000).tolist()
-    vs = rng.integers(0, k, 2000).tolist()
-    xs, ss, ys = cl.x.tolist(), cl.share.tolist(), cl.y.tolist()
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < min(3.0, budget_s / 4):
-        for u, v in zip(us, vs):
-            predictor_ref.predict_point(t_axes, vals, xs[u], ys[v], ss[u])
-        npairs += 2000
-    per_pair = (time.perf_counter() - t0) / npairs
-    # match sample
-    W = predictor_ref.predict_pairs_exact(t_axes, vals, cl.x, cl.share, cl.y)
-    Wp = np.where(W >= 1e-6, W, 0.0)
-    cost = Wp.max() - Wp
-    t0 = time.perf_counter()
-    matching_ref.solve_min_assignment(cost)
-    t_match = time.perf_counter() - t0
-    n_sq = max(n_target, m_target)
-    est_s = per_pair * n_target * m_target + t_match * (n_sq / k) ** 3
-    sample = (f"predict_point port timed on {npairs} pairs ({per_pair * 1e6:.2f} us/pair) x {n_target}*{m_target}; "
-              f"C Kuhn-Munkres port on a {k}x{k} predictor-derived round ({t_match:.2f} s) x ({n_sq}/{k})^3; "
-              f"1 thread; extrapolated to {n_target}x{m_target}")
-    return est_s * 1e3, sample, t_match + per_pair * npairs
+
+    def wfn(cl):
+        return predictor_ref.predict_pairs_exact(predictor_ref.DEFAULT_AXES, vals, cl.x, cl.share, cl.y)
+    measured["scipy_lsa_ms"] = {k: lsa_ms(make_cluster(k, k, seed=args.seed), wfn) for k in (1024, 2048)}
+    measured["round_64_ms"] = small
+    sample = f"{sample}; package from {os.path.relpath(ref_path, ROOT) if ref_path.startswith(ROOT) else ref_path}"
+    v = est
+    line = {"metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args),
+            "impl": "reference", "extrapolated": True,
+            "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "reference", "sample": sample,
+                             "cpu_model": cpu_model(), "nproc": os.cpu_count()},
+            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "measured": measured,
+            "pair_scores_per_s": args.n * args.m / (v / 1e3)}
+    print(json.dumps(line), flush=True)
 
 
 def ncu_traffic():
-    """DRAM bytes per launch of ssp_cluster_kernel from the committed ncu capture."""
-    for rnd in ("r01c", "r01b"):
+    """DRAM bytes per launch of the dominant kernel from the newest committed ncu capture."""
+    for rnd in ("r02", "r01c", "r01b"):
         try:
             with open(os.path.join(ROOT, "profiles", rnd, "ncu_cluster_traffic.json")) as f:
                 return json.load(f)["dram_bytes_per_launch"], rnd
@@ -176,26 +298,11 @@ def ncu_traffic():
     return None, None
 
 
-def run_reference(args, rank, world):
-    if rank != 0:
-        return
-    vals = []
-    sample = ""
-    for s in range(args.warmup + args.steps):
-        ms, sample, _ = cpu_reference(args.n, args.m, args.seed + s, budget_s=10.0)
-        if s >= args.warmup:
-            vals.append(ms)
-    v = float(np.mean(vals))
-    line = {"metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.n}x{args.m} scheduling round (predict + optimal match)",
-                       "n_online": args.n, "n_offline": args.m},
-            "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "ms", "cores": 1, "kind": "port", "sample": sample},
-            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "pair_scores_per_s": args.n * args.m / (v / 1e3)}
-    print(json.dumps(line), flush=True)
+def workload_config(args):
+    """Identical in both arms (the driver compares them)."""
+    return {"workload": f"{args.n}x{args.m} scheduling round (predict + optimal match)",
+            "n_online": args.n, "n_offline": args.m, "seed": args.seed,
+            "inputs": "synth.make_cluster(n, m, seed), default table; weight matrix (400 MB) > L2"}
 
 
 # ---------------------------------------------------------------------------
@@ -231,11 +338,11 @@ def run_ours(args, rank, world, local_rank):
     st = nat.MuxStats()
 
     def step():
-        nat.check(lib.mux_score_table(ctx, tb, xd.data_ptr(), sd.data_ptr(), n, yd.data_ptr(), m,
-                                      nat.MUX_SCORE_EXACT, nat.MUX_W_I32, q, Wq.data_ptr(), ldw, sptr))
-        # the online / offline SM demands order rows and columns for the solver's warm start
-        nat.check(lib.mux_match_keyed(ctx, Wq.data_ptr(), nat.MUX_W_I32, n, m, ldw, xd.data_ptr(), yd.data_ptr(),
-                                      col.data_ptr(), 0, nat.ctypes.byref(total), nat.ctypes.byref(st), sptr))
+        # one fused round on the HBM-resident snapshot: exact scoring into Wq,
+        # the multilevel solve (ordered by the online / offline SM demands), the
+        # tie canonicalisation
+        nat.check(lib.mux_round_dev(ctx, tb, xd.data_ptr(), sd.data_ptr(), n, yd.data_ptr(), m, q, Wq.data_ptr(), ldw,
+                                    col.data_ptr(), nat.ctypes.byref(total), nat.ctypes.byref(st), sptr))
         return st.as_dict(), int(total.value)
 
     for _ in range(args.warmup):
@@ -291,8 +398,9 @@ def run_ours(args, rank, world, local_rank):
             tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
-        e2e = {"value": e2e_ms / world, "unit": "ms", "h2d_bytes_per_step": (2 * n + m) * 8 * world,
-               "d2h_bytes_per_step": n * 4 * world, "per_round_ms": e2e_ms}
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": (2 * n + m) * 8,
+               "d2h_bytes_per_step": n * 4, "path": "mux_round C-ABI with host feature arrays (H2D + D2H in the timed region)",
+               "per_rank": True}
 
     # MLP plugin (tcgen05) scoring of the same N x M pairs: tensor-core roofline
     mlp_line = None
@@ -343,18 +451,35 @@ def run_ours(args, rank, world, local_rank):
     traffic, traffic_src = ncu_traffic()
     cpu = None
     if not args.no_cpu:
-        cpu_ms, sample, _ = cpu_reference(n, m, args.seed)
-        cpu = {"value": cpu_ms, "unit": "ms", "cores": 1, "kind": "port", "sample": sample}
+        got = load_reference()
+        if got is not None:
+            # bounded sample (~10 s): measured reference rounds at 128^2..512^2
+            with_aff = os.sched_getaffinity(0)
+            cores = pin_one_core()
+            cpu_ms, sample, measured = reference_estimate(got[0], n, m, args.seed, 256, 512)
+            os.sched_setaffinity(0, with_aff)
+            cpu = {"value": cpu_ms, "unit": "ms", "cores": cores, "kind": "reference", "sample": sample,
+                   "measured": measured, "extrapolated": True}
     s = stats_all[-1]
-    value = t_step / world
+    value = t_step
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", f"large_q{q}_{n}x{m}_s{args.seed}.json")
+    if rank == 0 and os.path.exists(gpath):
+        with open(gpath) as f:
+            gold = json.load(f)["total_q"]
+        parity = {"total_q": stats_all[-1]["total_q"], "golden_total_q": gold, "golden": os.path.relpath(gpath, ROOT),
+                  "match": stats_all[-1]["total_q"] == gold}
+        assert parity["match"], f"optimal total {stats_all[-1]['total_q']} != golden {gold}"
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32 (f64 scoring)", "data": "synthetic",
-        "config": {"workload": f"{n}x{m} scheduling round (predict + optimal match), replicas per GPU",
-                   "n_online": n, "n_offline": m, "qbits": q, "parallelism": f"replicas x{world}",
-                   "l2": "flushed (256 MB write) between timed steps; W (400 MB) > L2"},
-        "pair_scores_per_s": n * m * world / (t_step / 1e3),
+        "config": workload_config(args),
+        "run": {"qbits": q, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                "l2": "flushed (256 MB write) between timed steps; W (400 MB) > L2",
+                "multi_gpu": "each rank solves its own snapshot (seed + rank); value = per-round latency, max over ranks"},
+        "replica_rounds_per_s": world / (t_step / 1e3),
+        "pair_scores_per_s": n * m / (t_step / 1e3), "parity": parity,
         "roofline": {"bound": "hbm", "kernel": "ssp_cluster_kernel", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "traffic_note": f"DRAM read+write bytes per launch (ncu --set full, profiles/{traffic_src})",
@@ -363,7 +488,7 @@ def run_ours(args, rank, world, local_rank):
                      "note": "latency-bound: one dependent pop per step (sequential Dijkstra); bytes = 4*m per pop",
                      "share_of_step": dense_ms / t_step},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-        "gpu_launches": int(s["launches"]) + 3,
+        "gpu_launches": int(s["launches"]),
         "solver": {k: s[k] for k in ("levels", "par_steps", "dense_steps", "dense_searches", "dense_launches", "ms_dense", "ms_parallel",
                                      "row_scans", "total_q", "ms_match", "ms_canon", "canon_searches", "tight_edges",
                                      "dual_sweeps")},

@@ -199,6 +199,19 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table,
               int32_t* col_of_row_host, int64_t* total_q,
               mux_stats_t* stats, void* stream);
 
+/*
+ * mux_round on DEVICE-resident features (x_dev, share_dev [n], y_dev [m]):
+ * the same scoring + matching with the weights written to wq_dev ([n][ldw],
+ * int32 for qbits <= 30 else int64, rows 16-byte aligned; NULL = the
+ * context's own buffer) and col_of_row_dev (int32 [n], device).  Used when
+ * the features already live in HBM (a resident cluster snapshot).
+ */
+int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table,
+                  const double* x_dev, const double* share_dev, int64_t n,
+                  const double* y_dev, int64_t m, int qbits,
+                  void* wq_dev, int64_t ldw, int32_t* col_of_row_dev,
+                  int64_t* total_q, mux_stats_t* stats, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

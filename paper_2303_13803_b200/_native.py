@@ -20,7 +20,7 @@ MUX_SCORE_EXACT, MUX_SCORE_FAST = 0, 1
 # every symbol include/muxflow.h declares (checked by tests/test_native_abi.py)
 EXPORTS = ("mux_version", "mux_last_error", "mux_ctx_create", "mux_ctx_destroy",
            "mux_table_validate", "mux_score_table", "mux_score_mlp", "mux_match", "mux_match_keyed",
-           "mux_round")
+           "mux_round", "mux_round_dev")
 
 
 class MuxTable(ctypes.Structure):
@@ -90,6 +90,8 @@ def load():
                                         ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         lib.mux_round.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int, P,
                                   ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
+        lib.mux_round_dev.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int, P, i64, P,
+                                      ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         for name in EXPORTS[2:]:
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib

@@ -46,6 +46,49 @@ static int pinned_ensure(mux_ctx_t* ctx, size_t bytes) {
     ctx->pinned_bytes = cap;
     return MUX_OK;
 }
+struct EventPair {
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    ~EventPair() { for (auto& x : e) if (x) cudaEventDestroy(x); }
+};
+
+// Scoring + matching of one round on device-resident features.  wq_dev may be
+// null (the context's buffer is used); rowkey/colkey are HOST copies of x / y.
+static int round_device(mux_ctx_t* ctx, const mux_table_t* table, const double* x, const double* s, int64_t n,
+                        const double* y, int64_t m, int qbits, void* wq_dev, int64_t ldw, const double* rowkey,
+                        const double* colkey, int32_t* col_dev, int64_t* total_q, mux_stats_t* stats,
+                        cudaStream_t st) {
+    // weights are int32 up to 30 bits, int64 beyond (the exact-parity mode)
+    const int wt = qbits > 30 ? MUX_W_I64 : MUX_W_I32;
+    const int64_t esz = wt == MUX_W_I64 ? 8 : 4, vec = 16 / esz;
+    const int64_t ldw_min = ((m + vec - 1) / vec) * vec;
+    void* W = wq_dev;
+    if (W == nullptr) {
+        ldw = ldw_min;
+        MUX_TRY(ctx->wq.ensure((size_t)esz * (size_t)n * (size_t)(ldw > 0 ? ldw : vec)));
+        W = ctx->wq.ptr;
+    } else if (ldw < ldw_min || (ldw % vec) != 0 || (reinterpret_cast<uintptr_t>(W) & 15)) {
+        set_error("round: weight buffer rows must hold m entries, 16-byte aligned");
+        return MUX_EINVAL;
+    }
+    EventPair ev;
+    MUX_CUDA_TRY(cudaEventCreate(&ev.e[0]));
+    MUX_CUDA_TRY(cudaEventCreate(&ev.e[1]));
+    MUX_CUDA_TRY(cudaEventRecord(ev.e[0], st));
+    int64_t launches = 0;
+    if (m > 0)
+        MUX_TRY(mux_score_table_impl(ctx, table, x, s, n, y, m, MUX_SCORE_EXACT, wt, qbits, W, ldw, st, &launches));
+    MUX_CUDA_TRY(cudaEventRecord(ev.e[1], st));
+    MUX_TRY(check_flags(ctx, st));
+    float ms_score = 0.f;
+    cudaEventElapsedTime(&ms_score, ev.e[0], ev.e[1]);
+    MUX_TRY(mux_match_impl(ctx, W, wt, n, m, ldw, col_dev, total_q, stats, st, env_int("MUX_THETA", 4),
+                           env_int("MUX_TAIL", -1), rowkey, colkey));
+    if (stats) {
+        stats->ms_score = ms_score;
+        stats->launches += launches;
+    }
+    return MUX_OK;
+}
 }  // namespace mux
 
 using namespace mux;
@@ -223,9 +266,6 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     MUX_TRY(mux_table_validate(table));
     if (n < 0 || m < 0) { set_error("mux_round: bad shape"); return MUX_EINVAL; }
     if (qbits < 1 || qbits > 52) { set_error("mux_round: qbits must be in [1, 52]"); return MUX_EINVAL; }
-    // weights are int32 up to 30 bits, int64 beyond (the exact-parity mode)
-    const int wt = qbits > 30 ? MUX_W_I64 : MUX_W_I32;
-    const int64_t esz = wt == MUX_W_I64 ? 8 : 4, vec = 16 / esz;
     MUX_CUDA_TRY(cudaSetDevice(ctx->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (stats) memset(stats, 0, sizeof(*stats));
@@ -241,34 +281,34 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
     MUX_TRY(ctx->feat_in.ensure(fbytes));
     double* dfeat = ctx->feat_in.as<double>();
     MUX_CUDA_TRY(cudaMemcpyAsync(dfeat, hp, fbytes, cudaMemcpyHostToDevice, st));
-    const int64_t ldw = ((m + vec - 1) / vec) * vec;
-    MUX_TRY(ctx->wq.ensure((size_t)esz * (size_t)n * (size_t)(ldw > 0 ? ldw : vec)));
-    cudaEvent_t e0, e1;
-    MUX_CUDA_TRY(cudaEventCreate(&e0));
-    MUX_CUDA_TRY(cudaEventCreate(&e1));
-    MUX_CUDA_TRY(cudaEventRecord(e0, st));
-    int64_t launches = 0;
-    if (m > 0)
-        MUX_TRY(mux_score_table_impl(ctx, table, dfeat, dfeat + n, n, dfeat + 2 * n, m, MUX_SCORE_EXACT,
-                                     wt, qbits, ctx->wq.ptr, ldw, st, &launches));
-    MUX_CUDA_TRY(cudaEventRecord(e1, st));
-    MUX_TRY(check_flags(ctx, st));
-    float ms_score = 0.f;
-    cudaEventElapsedTime(&ms_score, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)n));
     int32_t* col_dev = ctx->colout.as<int32_t>();
-    // ordering keys for the multilevel solver: the online / offline SM demand
-    MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, wt, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1), x_host, y_host));
+    MUX_TRY(round_device(ctx, table, dfeat, dfeat + n, n, dfeat + 2 * n, m, qbits, nullptr, 0, x_host, y_host,
+                         col_dev, total_q, stats, st));
     MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_host, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
-    if (stats) {
-        stats->ms_score = ms_score;
-        stats->launches += launches;
-    }
     return MUX_OK;
+}
+
+int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev, const double* share_dev,
+                  int64_t n, const double* y_dev, int64_t m, int qbits, void* wq_dev, int64_t ldw,
+                  int32_t* col_of_row_dev, int64_t* total_q, mux_stats_t* stats, void* stream) {
+    if (!ctx) { set_error("null context"); return MUX_EINVAL; }
+    MUX_TRY(mux_table_validate(table));
+    if (n < 0 || m < 0) { set_error("mux_round_dev: bad shape"); return MUX_EINVAL; }
+    if (qbits < 1 || qbits > 52) { set_error("mux_round_dev: qbits must be in [1, 52]"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (total_q) *total_q = 0;
+    if (n == 0) return MUX_OK;
+    // host copies of the ordering keys (the solver sorts them on the host)
+    std::vector<double> rk(n), ck(m > 0 ? m : 1);
+    MUX_CUDA_TRY(cudaMemcpyAsync(rk.data(), x_dev, 8ull * n, cudaMemcpyDeviceToHost, st));
+    if (m) MUX_CUDA_TRY(cudaMemcpyAsync(ck.data(), y_dev, 8ull * m, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    return round_device(ctx, table, x_dev, share_dev, n, y_dev, m, qbits, wq_dev, ldw, rk.data(), ck.data(),
+                        col_of_row_dev, total_q, stats, st);
 }
 
 }  // extern "C"

@@ -82,6 +82,7 @@ struct Cnt {
     long long xcyc[4];   // exclusive kernel: pop, horizon re-scans, scan steps, augment
     int32_t xq, xretry;   // concurrent cluster searches: next deferred row, rows to retry
     unsigned long long xaborts;
+    unsigned long long xpfhits;   // register-key kernel: pops whose row slice was prefetched into smem
 };
 
 struct Lvl {
@@ -1285,6 +1286,247 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
 }
 
 // ---------------------------------------------------------------------------
+// register-key long-path kernel (the default for m <= CL * 512 * 4): the same
+// cluster Dijkstra as ssp_cluster_kernel's replicated push mode, with each
+// thread's tentative distances held in REGISTERS as ready-made sort keys.
+//
+// Thread t of CTA r owns columns c0 + t + u * NT (u < CC) for the whole
+// search, so their state never needs shared memory:
+//   kd[u] = (d_j << 24) | low_j           tentative distance as a sort key
+//   pk[u] = (p_j << 24) | low_j           price (constant during a search)
+//   low_j = (owned ? 1 << 23 : 0) | j     free columns first on ties, then lowest j
+// and relaxing row i at base distance b is one 64-bit add-subtract-compare:
+//   nk = (b << 24) + pk[u] - (a_ij << 24) = ((b + p_j - a_ij) << 24) | low_j.
+// A popped column gets bit 63 in both words: its nk then carries bit 63 and is
+// never below kd (nd >= the popped distance), and it drops out of the minimum.
+// Only the predecessor row stays in shared memory (the augmenting-path walk
+// reads it across the cluster).
+// ---------------------------------------------------------------------------
+
+constexpr uint64_t kTop = 1ull << 63;
+
+template <int CC, int CLS, int NT>
+__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1)
+ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ CShared S;
+    __shared__ __align__(16) CPush<CLS> P;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int32_t m = L.m;
+    const int32_t mc = (m + CLS - 1) / CLS;
+    const int rank = (int)cluster.block_rank();
+    const int32_t c0 = rank * mc;
+    const int32_t nloc = max(0, min(mc, m - c0));
+    int64_t* psr = reinterpret_cast<int64_t*>(smem);                          // [m] prices (replicated)
+    int32_t* rocr = reinterpret_cast<int32_t*>(psr + m);                      // [m] owners (replicated)
+    int32_t* pred = rocr + ((m + 1) & ~1);                                    // [mc] predecessor rows (local)
+    // two row-slice buffers for the runner-up prefetch (TMA bulk copies)
+    const int32_t slot_words = ((mc + 8 + 3) & ~3);
+    int32_t* rowbuf = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(pred + mc) + 127) & ~(uintptr_t)127);
+    __shared__ __align__(8) uint64_t pfbar[2];
+    __shared__ int32_t pfrow[2], pfshift[2];
+    __shared__ uint32_t pfpar[2];
+    const bool pf = (push & 4) != 0;
+    uint32_t pfcount[2] = {0, 0};   // tid 0: copies issued per slot
+    int cur = 0;
+    const int tid = threadIdx.x;
+    int par = 0;
+    uint32_t ph = 0;
+    uint64_t cand2 = kNoKey;
+    unsigned long long steps = 0, pfhits = 0;
+    const bool tm = (push & 16) != 0;
+    long long tcyc[3] = {0, 0, 0};
+    if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;
+    if (tid < 2) {
+        pfrow[tid] = -1;
+        pfshift[tid] = 0;
+        pfpar[tid] = 0;
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&pfbar[tid])) : "memory");
+    }
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    cpush_init<CLS, NT / 32>(P);
+    cluster.sync();
+    for (int32_t q = 0; q < ndef; ++q) {
+        const int32_t s = L.defer[q];
+        const int32_t* As = rowp(L, s);
+        for (int32_t j = tid; j < m; j += NT) {
+            psr[j] = __ldcg(L.p + j);
+            rocr[j] = __ldcg(L.roc + j);
+        }
+        __syncthreads();
+        uint64_t kd[CC], pk[CC];
+        int32_t as[CC];
+        // one reduction finds the source's profit (the largest a_sj - p_j) and
+        // the first pop (that column at distance 0; free columns first)
+        uint64_t vmin = kNoKey;
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * NT;
+            as[u] = jj < nloc ? __ldg(As + c0 + jj) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * NT;
+            if (jj < nloc) {
+                const int32_t j = c0 + jj;
+                const int64_t pj = psr[j];
+                if (pj < 0 || pj >= kDistLim) atomicOr(&L.cnt->errors, kErrDist);
+                const uint64_t low = (rocr[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                pk[u] = ((uint64_t)pj << 24) | low;
+                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << 24) | low;
+                vmin = k < vmin ? k : vmin;
+                pred[jj] = s;
+            } else {
+                pk[u] = kTop;
+            }
+        }
+        const uint64_t k0 = cluster_min_push<CLS, NT / 32>(vmin, S, P, par, ph, rank, cand2);
+        const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * NT;
+            kd[u] = jj < nloc ? (((uint64_t)pis << 24) + pk[u] - ((uint64_t)(uint32_t)as[u] << 24)) : kNoKey;
+        }
+        uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
+        int32_t jf;
+        int64_t D;
+        int32_t pops = 0;
+        bool abandon = false;
+        while (true) {
+            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
+            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t i = rocr[jm];
+            if (i < 0) { jf = jm; D = dmin; break; }
+            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            const long long tA = tm ? clock64() : 0;
+            const int32_t* Ai = rowp(L, i);
+            const int64_t aim = (int64_t)__ldg(Ai + jm);
+            int32_t av[CC];
+            if (pf && pfrow[cur] == i) {
+                // the runner-up of the previous step: its slice is (being) copied into smem
+                const uint32_t bar = smem_u32(&pfbar[cur]), parity = pfpar[cur];
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+                const int32_t* rb = rowbuf + cur * slot_words + pfshift[cur];
+#pragma unroll
+                for (int u = 0; u < CC; ++u) {
+                    const int32_t jj = tid + u * NT;
+                    av[u] = jj < nloc ? rb[jj] : 0;
+                }
+                ++pfhits;
+            } else {
+#pragma unroll
+                for (int u = 0; u < CC; ++u) {
+                    const int32_t jj = tid + u * NT;
+                    av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
+                }
+            }
+            // runner-up prefetch: warp 0 copies this CTA's slice of the row owning the
+            // runner-up column (often the next pop) into the other buffer by TMA
+            if (pf && tid < 32) {
+                const uint64_t k2 = wmin64(cand2);
+                const int nb = cur ^ 1;
+                if (tid == 0 && k2 != kNoKey && nloc > 0) {
+                    const int32_t i2 = rocr[k2 & 0x7FFFFFu];
+                    if (i2 >= 0 && i2 != pfrow[nb]) {
+                        const uint32_t bar = smem_u32(&pfbar[nb]);
+                        if (pfcount[nb] > 0) {
+                            // the buffer's previous copy must have landed before it is rewritten
+                            const uint32_t parity = (pfcount[nb] - 1) & 1u;
+                            uint32_t done = 0;
+                            while (!done)
+                                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                             : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+                        }
+                        const int32_t* src = rowp(L, i2) + c0;
+                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+                        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
+                        const uint32_t bytes = (uint32_t)(a1 - a0);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                     ::"r"(smem_u32(rowbuf + nb * slot_words)), "l"(a0), "r"(bytes), "r"(bar) : "memory");
+                        pfpar[nb] = pfcount[nb] & 1u;
+                        ++pfcount[nb];
+                        pfrow[nb] = i2;
+                        pfshift[nb] = (int32_t)((reinterpret_cast<uintptr_t>(src) - a0) >> 2);
+                    }
+                }
+            }
+            // pop jm: its owner thread marks it scanned
+            if (jm >= c0 && jm < c0 + nloc) {
+#pragma unroll
+                for (int u = 0; u < CC; ++u)
+                    if (jm - c0 == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+            }
+            const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << 24;
+            best = kNoKey;
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const uint64_t nk = base + pk[u] - ((uint64_t)(uint32_t)av[u] << 24);
+                if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
+                best = kd[u] < best ? kd[u] : best;
+            }
+            const long long tB = tm ? clock64() : 0;
+            best = cluster_min_push<CLS, NT / 32>(best, S, P, par, ph, rank, cand2);
+            if (tm) {
+                const long long tC = clock64();
+                tcyc[0] += tB - tA;
+                tcyc[1] += tC - tB;
+                tcyc[2] += 1;
+            }
+            cur ^= 1;
+            ++steps;
+        }
+        if (!abandon) {
+            // dual update on the local scanned columns: p_j += D - d_j
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t jj = tid + u * NT;
+                if (jj < nloc && (kd[u] & kTop)) {
+                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> 24), dj = (int64_t)((kd[u] & ~kTop) >> 24);
+                    L.p[c0 + jj] = pj + (D - dj);
+                }
+            }
+            // the path: predecessors live in their owners' shared memory
+            if (rank == 0 && tid == 0) {
+                int32_t j = jf;
+                while (true) {
+                    const int owner = j / mc;
+                    const int32_t ii = cluster.map_shared_rank(pred, owner)[j - owner * mc];
+                    const int32_t jn = (ii == s) ? -1 : __ldcg(L.cor + ii);
+                    L.roc[j] = ii;
+                    L.cor[ii] = j;
+                    if (ii == s) break;
+                    j = jn;
+                }
+            }
+        }
+        __threadfence();
+        cluster.sync();
+    }
+    // no bulk copy may still be writing this CTA's shared memory at exit
+    if (tid == 0)
+        for (int b = 0; b < 2; ++b)
+            if (pfcount[b] > 0) {
+                const uint32_t bar = smem_u32(&pfbar[b]), parity = (pfcount[b] - 1) & 1u;
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+            }
+    if (rank == 0 && tid == 0) {
+        atomicAdd(&L.cnt->xsteps, steps);
+        atomicAdd(&L.cnt->xpfhits, pfhits);
+    }
+    if (tm && rank == 0 && tid == 0)
+        for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
+}
+
+// ---------------------------------------------------------------------------
 // level setup kernels
 // ---------------------------------------------------------------------------
 
@@ -1565,6 +1807,10 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 8, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<1, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<2, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     // threads per CTA of the replicated long-path cluster kernel: 512 (4 columns per
     // thread) by default -- fewer warps to reduce and to wait for at each pop's CTA
     // barrier; 256 / 1024 selectable (all cover m <= 16,384)
@@ -1577,7 +1823,9 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     // MUX_SSP_PF: 0 off, 1 runner-up row (default), 2 every warp-0 lane's candidate row
     const int pf_mode = getenv("MUX_SSP_PF") ? atoi(getenv("MUX_SSP_PF")) : 1;
     const bool cpf = cpush_mode == 1 && pf_mode > 0;
-    const int32_t cpush = cpush_mode | (cpf ? 4 : 0) | (cpf && pf_mode == 2 ? 8 : 0);
+    const int32_t cpush = cpush_mode | (cpf ? 4 : 0) | (cpf && pf_mode == 2 ? 8 : 0) | (getenv("MUX_SSP_TIME") ? 16 : 0);
+    // long paths on the register-key kernel (MUX_SSP_RKEY=0: the shared-memory kernel)
+    const bool use_rkey = !(getenv("MUX_SSP_RKEY") && *getenv("MUX_SSP_RKEY") == '0');
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
@@ -1697,9 +1945,18 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const int32_t pl = l == 0 ? 0 : coarse_pops;
             const bool repl_ok = use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048 - push_b8;
             const bool shard_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
+            // register-key kernel: 12 m replicated + 4 bytes per local column
+            const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * 4 * ((mcl + 8 + 3) & ~3) + 64;
+            const bool rkey_ok = use_rkey && use_cluster && cpush_mode == 1 && mcl <= 512 * 4 &&
+                                 rk_bytes <= xs_budget - 2048 - push_b8;
             auto launch_cl = [&](int32_t nrows, int32_t conc, int32_t nclusters) {
                 const unsigned g = (unsigned)(CL * nclusters);
-                if (repl_ok) {
+                if (rkey_ok && !conc) {
+                    if (mcl <= 512) ssp_rkey_kernel<1, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
+                    else if (mcl <= 1024) ssp_rkey_kernel<2, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
+                    else if (mcl <= 1536) ssp_rkey_kernel<3, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
+                    else ssp_rkey_kernel<4, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
+                } else if (repl_ok) {
                     if (cl_size == 16 && !conc && 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64 <= xs_budget - 2048 - push_b16)
                         ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0, cpush);
                     else if (cl_size == 4 && !conc)
@@ -1830,5 +2087,10 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     for (auto& e : ev) cudaEventDestroy(e);
     if (verbose) fprintf(stderr, "[ssp] n %d levels %d total %.3f ms (host wall), dense %.3f ms, parallel %.3f ms\n", n, nl, ms,
                          ms_dense, ms_par);
+    if (cpush & 16) {
+        const double k = hc.xcyc[2] > 0 ? (double)hc.xcyc[2] : 1.0;
+        fprintf(stderr, "[ssp-time] pops %lld cycles/pop (CTA 0 warp 0): load+relax %.0f exchange %.0f | prefetch hits %.3f\n",
+                (long long)hc.xcyc[2], hc.xcyc[0] / k, hc.xcyc[1] / k, (double)hc.xpfhits / (double)std::max(1ull, hc.xsteps));
+    }
     return MUX_OK;
 }
