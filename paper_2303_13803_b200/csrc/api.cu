@@ -21,9 +21,60 @@ namespace mux {
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
 
-static int env_int(const char* name, int dflt) {
+namespace {
+// Integer knob in [lo, hi]; a malformed or out-of-range value sets the error.
+int knob(const char* name, int dflt, long lo, long hi, std::string& err) {
     const char* v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
+    if (!v || !*v) return dflt;
+    char* end = nullptr;
+    const long x = strtol(v, &end, 10);
+    if (*end != '\0' || x < lo || x > hi) {
+        if (err.empty()) err = std::string(name) + "=" + v + " outside [" + std::to_string(lo) + ", " + std::to_string(hi) + "]";
+        return dflt;
+    }
+    return (int)x;
+}
+}  // namespace
+
+const Tuning& tuning() {
+    static thread_local Tuning t;
+    t = Tuning{};
+    std::string err;
+    t.verbose = getenv("MUX_VERBOSE") != nullptr;
+    t.ssp_check = knob("MUX_SSP_CHECK", 0, 0, 1, err) == 1;
+    t.ssp_time = knob("MUX_SSP_TIME", 0, 0, 1, err) == 1;
+    if (knob("MUX_TUNING", 0, 0, 1, err) == 1) {
+        const char* sv = getenv("MUX_SOLVER");
+        if (sv && *sv) {
+            if (strcmp(sv, "auction") == 0) t.force_auction = true;
+            else if (strcmp(sv, "ssp") != 0 && err.empty()) err = std::string("MUX_SOLVER=") + sv + " (auction | ssp)";
+        }
+        t.canon = knob("MUX_CANON", 1, 0, 1, err) == 1;
+        t.ssp_rect = knob("MUX_SSP_RECT", 1, 0, 1, err) == 1;
+        t.ssp_f = knob("MUX_SSP_F", t.ssp_f, 2, 16, err);
+        t.ssp_base = knob("MUX_SSP_BASE", t.ssp_base, 8, 4096, err);
+        t.ssp_steps = knob("MUX_SSP_STEPS", t.ssp_steps, 1, 100000, err);
+        t.ssp_deep = knob("MUX_SSP_DEEP", t.ssp_deep, 0, 1000, err);
+        t.ssp_coarse_pops = knob("MUX_SSP_COARSE_POPS", 0, 0, 1000000000, err);
+        t.ssp_serial = knob("MUX_SSP_SERIAL", 0, 0, 1, err) == 1;
+        t.ssp_pf = knob("MUX_SSP_PF", 1, 0, 1, err) == 1;
+        t.ssp_cluster = knob("MUX_SSP_CLUSTER", 1, 0, 1, err) == 1;
+        t.ssp_sparsex = knob("MUX_SSP_SPARSEX", 0, 0, 1, err) == 1;
+        t.auc_theta = knob("MUX_THETA", t.auc_theta, 2, 64, err);
+        t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 16, err);
+        t.auc_k = knob("MUX_K", t.auc_k, 1, 15, err);
+        t.auc_cg_sync = knob("MUX_CG_SYNC", 1, 0, 1, err) == 1;
+        t.auc_async_tail = knob("MUX_ASYNC_TAIL", -1, -1, 1, err);
+        t.auc_async_phases = knob("MUX_ASYNC_PHASES", t.auc_async_phases, 0, 1 << 20, err);
+        t.auc_fresh = knob("MUX_FRESH", 1, 0, 2, err);
+        t.auc_restage = knob("MUX_RESTAGE", 0, 0, 2, err);
+        t.auc_order = knob("MUX_ORDER", 1, 0, 2, err);
+        t.auc_no_smem = knob("MUX_NO_SMEM", 0, 0, 1, err) == 1;
+        t.mlp_prefetch = knob("MUX_MLP_PREFETCH", 0, 0, 1, err) == 1;
+    }
+    t.error = !err.empty();
+    if (t.error) set_error("bad tuning knob: " + err);
+    return t;
 }
 
 // Read back and clear the device error flags; maps a range error to EINVAL.
@@ -81,8 +132,8 @@ static int round_device(mux_ctx_t* ctx, const mux_table_t* table, const double* 
     MUX_TRY(check_flags(ctx, st));
     float ms_score = 0.f;
     cudaEventElapsedTime(&ms_score, ev.e[0], ev.e[1]);
-    MUX_TRY(mux_match_impl(ctx, W, wt, n, m, ldw, col_dev, total_q, stats, st, env_int("MUX_THETA", 4),
-                           env_int("MUX_TAIL", -1), rowkey, colkey));
+    MUX_TRY(mux_match_impl(ctx, W, wt, n, m, ldw, col_dev, total_q, stats, st, tuning().auc_theta,
+                           tuning().auc_tail, rowkey, colkey));
     if (stats) {
         stats->ms_score = ms_score;
         stats->launches += launches;
@@ -125,7 +176,7 @@ int mux_ctx_destroy(mux_ctx_t* ctx) {
     if (!ctx) return MUX_OK;
     cudaSetDevice(ctx->device);
     for (DevBuf* b : {&ctx->table, &ctx->rowfeat, &ctx->colfeat, &ctx->flags, &ctx->feat_in, &ctx->wq,
-                      &ctx->colout, &ctx->auc, &ctx->ssp, &ctx->canon, &ctx->mlp})
+                      &ctx->colout, &ctx->auc, &ctx->ssp, &ctx->canon, &ctx->canon_ent, &ctx->mlp})
         b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     delete ctx;
@@ -148,6 +199,8 @@ int mux_table_validate(const mux_table_t* t) {
     }
     if (!t->values) { set_error("table values missing"); return MUX_EINVAL; }
     const int64_t nv = (int64_t)dims[0] * dims[1] * dims[2];
+    // table offsets are int32 on the device (csrc/score.cu)
+    if (nv > (int64_t)INT32_MAX) { set_error("table has more than 2^31 - 1 values"); return MUX_EINVAL; }
     double lo = INFINITY, hi = -INFINITY;
     for (int64_t e = 0; e < nv; ++e) {
         const double v = t->values[e];
@@ -220,7 +273,7 @@ int mux_match(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, int64_t 
     }
     if (stats) memset(stats, 0, sizeof(*stats));
     MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1), nullptr, nullptr));
+                           tuning().auc_theta, tuning().auc_tail, nullptr, nullptr));
     if (out_on_host && n > 0) {
         MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));
@@ -250,7 +303,7 @@ int mux_match_keyed(mux_ctx_t* ctx, const void* Wq_dev, int wtype, int64_t n, in
     }
     if (stats) memset(stats, 0, sizeof(*stats));
     MUX_TRY(mux_match_impl(ctx, Wq_dev, wtype, n, m, ldw, col_dev, total_q, stats, st,
-                           env_int("MUX_THETA", 4), env_int("MUX_TAIL", -1),
+                           tuning().auc_theta, tuning().auc_tail,
                            rk.empty() ? nullptr : rk.data(), ck.empty() ? nullptr : ck.data()));
     if (out_on_host && n > 0) {
         MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_out, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));

@@ -1385,10 +1385,6 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
                    int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
                    cudaStream_t st, mux_stats_t* stats);
 
-static int env_flag(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
-}
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -1416,16 +1412,16 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         }
     }
     if (total_q) *total_q = 0;
+    const Tuning& T = tuning();
+    if (T.error) return MUX_EINVAL;
     if (n == 0) return MUX_OK;
     {
-        // Square int32 problems: multilevel shortest-path solver (csrc/ssp.cu);
-        // MUX_SOLVER=auction selects the epsilon-scaling auction below.
-        const char* sv = getenv("MUX_SOLVER");
+        // int32 problems: multilevel shortest-path solver (csrc/ssp.cu);
+        // int64 (qbits > 30) and MUX_SOLVER=auction: the epsilon-scaling auction below.
         // N < M: the zero padding rows of the reference's square problem are
-        // implicit; N > M (more online rows than jobs) stays on the auction
-        const bool rect_ok = !(getenv("MUX_SSP_RECT") && *getenv("MUX_SSP_RECT") == '0');
-        const bool use_ssp_t = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && M >= 1 && N >= 2 &&
-                               N > M && rect_ok;
+        // implicit; N > M: the transposed problem (jobs as rows)
+        const bool rect_ok = T.ssp_rect;
+        const bool use_ssp_t = !T.force_auction && wtype == MUX_W_I32 && M >= 1 && N >= 2 && N > M && rect_ok;
         if (use_ssp_t) {
             // N > M: solve the transposed M x N problem (jobs as rows, the padding
             // columns of the reference become implicit zero rows), then map the
@@ -1453,8 +1449,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             // column (job) prices = the transposed rows' profits
             untranspose_duals_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(WT, ldt, mm, nn, pT, corT, rocT,
                                                                                  (int64_t)nn + 1, colr, price, owner);
-            const char* cs = getenv("MUX_CANON");
-            if (!(cs && *cs == '0'))
+            if (T.canon)
                 MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, mm, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats));
             finalize_ssp_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
                 static_cast<const int32_t*>(W), ldw, nn, mm, colr, col_out_dev);
@@ -1464,7 +1459,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             if (total_q) *total_q = tq;
             return MUX_OK;
         }
-        const bool use_ssp = !(sv && strcmp(sv, "auction") == 0) && wtype == MUX_W_I32 && N >= 1 && M >= 2 &&
+        const bool use_ssp = !T.force_auction && wtype == MUX_W_I32 && N >= 1 && M >= 2 &&
                              (N == M || (N < M && rect_ok));
         if (use_ssp) {
             const int32_t nn = (int32_t)M;
@@ -1477,8 +1472,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             int64_t tq = 0;
             MUX_TRY(mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, rowkey, colkey, col_out_dev,
                                  &tq, price, colr, owner, stats, st));
-            const char* cs = getenv("MUX_CANON");
-            if (!(cs && *cs == '0')) {
+            if (T.canon) {
                 // canonicalisation works in the auction's units: benefits Q * (n + 1)
                 scale_price_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(price, nn, (int64_t)nn + 1);
                 MUX_TRY(mux_canon_impl(ctx, W, wtype, (int32_t)N, nn, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st,
@@ -1567,30 +1561,23 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     A.eps0 = (int64_t)(maxa / 4.0);
     if (A.eps0 < 1) A.eps0 = 1;
     A.round_guard = 200000000ll;
-    const char* cgs = getenv("MUX_CG_SYNC");
-    A.cg_sync = (cgs && *cgs == '0') ? 0 : 1;   // cooperative-groups grid.sync measured faster
+    A.cg_sync = T.auc_cg_sync ? 1 : 0;   // cooperative-groups grid.sync measured faster
     A.rot = (N != M) ? 1 : 0;
-    const char* as = getenv("MUX_ASYNC_TAIL");      // default: on for n >= 512
-    A.async_tail = (as && *as) ? (*as == '1') : (n >= 512);
+    A.async_tail = T.auc_async_tail >= 0 ? T.auc_async_tail : (n >= 512);   // default: on for n >= 512
     if (A.tail_max < 0) A.tail_max = 16;
-    const char* ap = getenv("MUX_ASYNC_PHASES");
     // with the concurrent chains on, every phase runs as chains (no Jacobi
     // rounds): on near-rank-1 weights a Jacobi round settles ~1 person when
     // everyone bids for the same object (10k: 9,400 rounds in phase 0)
-    A.async_phases = (ap && *ap) ? atoi(ap) : 1 << 20;
-    A.fresh = env_flag("MUX_FRESH", 1);
-    A.restage = env_flag("MUX_RESTAGE", 0);
-    A.order = env_flag("MUX_ORDER", 1);     // auto (measured best for both tail modes at 10k)
-    const char* ks = getenv("MUX_K");
-    A.keff = (ks && *ks) ? atoi(ks) : kK;
-    if (A.keff < 1) A.keff = 1;
-    if (A.keff > kK) A.keff = kK;
+    A.async_phases = T.auc_async_phases;
+    A.fresh = T.auc_fresh;
+    A.restage = T.auc_restage;
+    A.order = T.auc_order;     // auto (measured best for both tail modes at 10k)
+    A.keff = std::min(std::max(T.auc_k, 1), kK);
 
     // shared memory: two row buffers + price/owner mirrors when they fit
     const size_t rows_bytes = 2ull * (size_t)row_bytes;
     const size_t mirror = (size_t)n_pad * (sizeof(int64_t) + sizeof(int32_t));
-    const char* no_smem = getenv("MUX_NO_SMEM");   // test hook: force the global-memory path
-    const bool smem_mode = rows_bytes + mirror + sizeof(Shared) + 1024 <= kSmemBudget && !(no_smem && *no_smem == '1');
+    const bool smem_mode = rows_bytes + mirror + sizeof(Shared) + 1024 <= kSmemBudget && !T.auc_no_smem;
     const size_t dsmem = smem_mode ? rows_bytes + mirror : 0;
     void* fn;
     if (wtype == MUX_W_I32) fn = smem_mode ? (void*)auction_kernel<MUX_W_I32, true> : (void*)auction_kernel<MUX_W_I32, false>;
@@ -1601,9 +1588,13 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     if (per_sm < 1) { set_error("auction kernel cannot be resident"); return MUX_ECUDA; }
     dim3 grid((unsigned)ctx->num_sms), block(kAucThreads);
     void* args[] = {&A};
-    cudaEvent_t e0, e1;
-    MUX_CUDA_TRY(cudaEventCreate(&e0));
-    MUX_CUDA_TRY(cudaEventCreate(&e1));
+    struct Events {   // destroyed on every exit path
+        cudaEvent_t a = nullptr, b = nullptr;
+        ~Events() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+    } evs;
+    MUX_CUDA_TRY(cudaEventCreate(&evs.a));
+    MUX_CUDA_TRY(cudaEventCreate(&evs.b));
+    cudaEvent_t e0 = evs.a, e1 = evs.b;
     MUX_CUDA_TRY(cudaEventRecord(e0, st));
     MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, grid, block, args, dsmem, st));
     ++launches;
@@ -1611,8 +1602,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     {
         // among all optimal assignments, return the one the reference's
         // canonicalisation emits (csrc/canon.cu); MUX_CANON=0 skips it
-        const char* cs = getenv("MUX_CANON");
-        if (!(cs && *cs == '0') && N > 0 && M > 0) {
+        if (T.canon && N > 0 && M > 0) {
             MUX_CUDA_TRY(cudaStreamSynchronize(st));
             AucCounters pre;
             MUX_CUDA_TRY(cudaMemcpy(&pre, A.cnt, sizeof(pre), cudaMemcpyDeviceToHost));
@@ -1635,8 +1625,6 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     if (hc.errors & kErrIterGuard) { set_error("auction: round guard tripped"); return MUX_ELIMIT; }
     if (hc.errors & kErrPriceBits) { set_error("auction: price overflowed its packing"); return MUX_ELIMIT; }
     if (total_q) *total_q = hc.total_q;
@@ -1650,7 +1638,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         stats->ms_kernel = hc.ns_total * 1e-6;
         stats->cache_hits = (int64_t)hc.hits;
         stats->launches += launches;
-        if (getenv("MUX_VERBOSE")) {
+        if (T.verbose) {
             fprintf(stderr, "[mux] async-tail rejected bids: %llu\n", hc.async_fail);
             unsigned long long prev = 0;
             for (int k = 0; k < (int)hc.phases && k < kPhMax; ++k) {
@@ -1661,14 +1649,14 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
                 prev = hc.ph_bids[k];
             }
         }
-        if (getenv("MUX_VERBOSE"))
+        if (T.verbose)
             fprintf(stderr, "[mux] tail: hits %llu hit-loop cycles/hit %.0f; fetch cycles/scan %.0f\n", hc.tail_hits,
                     hc.cyc_hitloop / (double)(hc.tail_hits + 1), hc.cyc_fetch / (double)(hc.tail_scans + 1));
-        if (getenv("MUX_VERBOSE"))
+        if (T.verbose)
             fprintf(stderr, "[mux] tail: scans %llu hit_ms %.2f scan_ms %.2f wait_ms %.2f | rounds: a1 %.2f a2 %.2f b %.2f ms\n",
                     hc.tail_scans, hc.ns_tail_hit * 1e-6, hc.ns_tail_scan * 1e-6, hc.ns_tail_wait * 1e-6,
                     hc.ns_a1 * 1e-6, hc.ns_a2 * 1e-6, hc.ns_b * 1e-6);
-        if (getenv("MUX_VERBOSE"))
+        if (T.verbose)
             fprintf(stderr, "[mux] CTA0 scans %lld, cycles/scan: pass1 %.0f tau %.0f pass2 %.0f rank %.0f store %.0f\n",
                     hc.ns_stage[5], hc.ns_stage[0] / (double)(hc.ns_stage[5] + 1), hc.ns_stage[1] / (double)(hc.ns_stage[5] + 1),
                     hc.ns_stage[2] / (double)(hc.ns_stage[5] + 1), hc.ns_stage[3] / (double)(hc.ns_stage[5] + 1),

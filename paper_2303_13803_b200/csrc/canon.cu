@@ -344,8 +344,9 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
                    cudaStream_t st, mux_stats_t* stats) {
     if (N <= 0 || M <= 0 || n <= 0) return MUX_OK;
     const auto h0 = std::chrono::steady_clock::now();
-    int64_t cap = (int64_t)N * (int64_t)M;
-    if (cap > (1ll << 28)) cap = 1ll << 28;
+    // default tight-edge buffer: ~4 n edges in a predictor round; a round with
+    // more (many equal scores) is re-run at its exact count below
+    int64_t cap = std::min<int64_t>((int64_t)N * (int64_t)M, 64ll * n + 1024);
     if (cap < 16) cap = 16;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) & ~(size_t)255; return o; };
@@ -390,7 +391,23 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     const auto h1 = std::chrono::steady_clock::now();
     if (hc.errors & kCanonErrGuard) { set_error("canonicalisation: dual repair did not converge"); return MUX_ELIMIT; }
-    if (hc.errors & kCanonErrCap) { set_error("canonicalisation: tight-edge graph exceeds its buffer"); return MUX_ELIMIT; }
+    if (hc.errors & kCanonErrCap) {
+        // more tight edges than the default buffer holds (many equal scores):
+        // the count pass already has the exact total -- size for it and rerun
+        const int64_t need = (int64_t)hc.tight_total;
+        if (need > (int64_t)N * (int64_t)M) { set_error("canonicalisation: tight-edge count out of range"); return MUX_ELIMIT; }
+        MUX_TRY(ctx->canon_ent.ensure(4ull * (size_t)need + 256));
+        C.ent = ctx->canon_ent.as<int32_t>();
+        C.cap = need;
+        MUX_CUDA_TRY(cudaMemsetAsync(&C.cnt->tight_total, 0, sizeof(unsigned long long), st));
+        MUX_CUDA_TRY(cudaMemsetAsync(&C.cnt->errors, 0, sizeof(uint32_t), st));
+        if (wtype == MUX_W_I32) tight_kernel<MUX_W_I32><<<tg, 256, 0, st>>>(C);
+        else tight_kernel<MUX_W_I64><<<tg, 256, 0, st>>>(C);
+        MUX_CUDA_TRY(cudaGetLastError());
+        MUX_CUDA_TRY(cudaMemcpyAsync(&hc, C.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaStreamSynchronize(st));
+        if (hc.errors & kCanonErrCap) { set_error("canonicalisation: tight-edge graph exceeds its buffer"); return MUX_ELIMIT; }
+    }
 
     std::vector<int32_t> col(n), rcnt(N), ent((size_t)hc.tight_total);
     std::vector<int64_t> p(n), u(n), roff(N);
@@ -422,7 +439,7 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
     Canon K(G, col);
     K.run();
     const auto h3 = std::chrono::steady_clock::now();
-    if (getenv("MUX_VERBOSE")) {
+    if (tuning().verbose) {
         auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
             return std::chrono::duration<double, std::milli>(b - a).count();
         };

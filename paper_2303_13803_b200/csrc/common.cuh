@@ -40,6 +40,44 @@ enum : uint32_t {
     kErrIterGuard = 1u << 2,    // auction round guard tripped
 };
 
+// Every environment knob the library reads, parsed and range-checked in one
+// place (tuning() in csrc/api.cu, re-read on each call).  Diagnostics are
+// always honoured; everything that changes which kernels run or how is an
+// experiment knob, honoured only under MUX_TUNING=1, so a stray variable in a
+// production environment cannot change the solver.  An out-of-range value is
+// an error (mux_last_error names it), not silently clamped.
+struct Tuning {
+    // diagnostics (always)
+    bool verbose = false;        // MUX_VERBOSE: per-level solver log on stderr
+    bool ssp_check = false;      // MUX_SSP_CHECK=1: dense dual certificate after every level
+    bool ssp_time = false;       // MUX_SSP_TIME=1: per-pop cycle split of the long-path kernel
+    // experiments (MUX_TUNING=1 only)
+    bool force_auction = false;  // MUX_SOLVER=auction: epsilon-scaling auction for int32 too
+    bool canon = true;           // MUX_CANON=0: skip the tie canonicalisation
+    bool ssp_rect = true;        // MUX_SSP_RECT=0: rectangular rounds on the auction
+    int ssp_f = 2;               // MUX_SSP_F [2, 16]: coarsening factor between levels
+    int ssp_base = 48;           // MUX_SSP_BASE [8, 4096]: size of the coarsest level
+    int ssp_steps = 48;          // MUX_SSP_STEPS [1, 100000]: pops before a warp search is deferred
+    int ssp_deep = 4;            // MUX_SSP_DEEP [0, 1000]: dense re-scans before deferral
+    int ssp_coarse_pops = 0;     // MUX_SSP_COARSE_POPS [0, 1e9]: long-search pop limit at coarse levels
+    bool ssp_serial = false;     // MUX_SSP_SERIAL=1: one warp search at a time
+    bool ssp_pf = true;          // MUX_SSP_PF=0: no runner-up row prefetch in the long-path kernel
+    bool ssp_cluster = true;     // MUX_SSP_CLUSTER=0: single-CTA / single-warp long paths
+    bool ssp_sparsex = false;    // MUX_SSP_SPARSEX=1: single-warp sparse long paths
+    int auc_theta = 4;           // MUX_THETA [2, 64]: epsilon-scaling factor
+    int auc_tail = -1;           // MUX_TAIL [-1, 16]: unassigned count that ends the Jacobi rounds
+    int auc_k = 15;              // MUX_K [1, 15]: cached candidates per bidder
+    bool auc_cg_sync = true;     // MUX_CG_SYNC=0: custom grid barrier
+    int auc_async_tail = -1;     // MUX_ASYNC_TAIL [-1, 1]: concurrent tail chains (-1 = n >= 512)
+    int auc_async_phases = 1 << 20;   // MUX_ASYNC_PHASES [0, 2^20]
+    int auc_fresh = 1, auc_restage = 0, auc_order = 1;   // MUX_FRESH / MUX_RESTAGE / MUX_ORDER [0, 2]
+    bool auc_no_smem = false;    // MUX_NO_SMEM=1: global-memory auction path
+    bool mlp_prefetch = false;   // MUX_MLP_PREFETCH=1
+    bool error = false;          // an out-of-range value was given
+};
+// Current knob values; *err set to a message when a value is out of range.
+const Tuning& tuning();
+
 // Grow-only device buffer.
 struct DevBuf {
     void* ptr = nullptr;
@@ -86,6 +124,7 @@ struct mux_ctx {
     mux::DevBuf ssp;
     // tie canonicalisation workspace (duals, tight-edge CSR)
     mux::DevBuf canon;
+    mux::DevBuf canon_ent;  // tight-edge CSR entries when they outgrow the default buffer
     // MLP plugin parameters + layer-1 partials
     mux::DevBuf mlp;
     size_t auc_n = 0;

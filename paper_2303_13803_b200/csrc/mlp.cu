@@ -386,8 +386,7 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
     p.n = (int32_t)n; p.m = (int32_t)m;
     const int64_t tiles = n * ((m + kTile - 1) / kTile);
     if (tiles > 0) {
-        const char* pv = getenv("MUX_MLP_PREFETCH");
-        const bool pf = pv && *pv == '1';
+        const bool pf = tuning().mlp_prefetch;
         const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * (pf ? MlpCfg<true>::ctas : MlpCfg<false>::ctas));
         const double qscale = ldexp(1.0, qbits);
         if (pf) {

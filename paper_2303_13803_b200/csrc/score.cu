@@ -21,6 +21,8 @@
 // columns of one row (one 16-byte store for 32-bit outputs, two for 64-bit),
 // a CTA covers 1024 columns x kRowsPerCta rows.  Padding columns [m, ldo) of
 // quantised outputs are written as 0 so row scans can read whole vectors.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace mux {
@@ -163,7 +165,9 @@ score_exact_kernel(DevTable t, const RowFeat* __restrict__ rf, const ColFeat* __
 #pragma unroll
     for (int q = 0; q < 4; ++q) { cj[q][0] = c[q].j0 * nk; cj[q][1] = c[q].j1 * nk; }
     const int32_t njk = nj * nk;
-    const int64_t row_begin = (int64_t)blockIdx.y * kRowsPerCta;
+    // grid-stride over row blocks: grid.y is capped at 65535
+    for (int64_t rb = blockIdx.y; rb * kRowsPerCta < n; rb += gridDim.y) {
+    const int64_t row_begin = rb * kRowsPerCta;
     const int64_t row_end = min(n, row_begin + kRowsPerCta);
     for (int64_t row = row_begin; row < row_end; ++row) {
         const RowFeat r = rf[row];
@@ -191,6 +195,7 @@ score_exact_kernel(DevTable t, const RowFeat* __restrict__ rf, const ColFeat* __
         if (col0 + 4 <= ldo) store4<WT>(out, ldo, row, col0, w, true, qscale);
         else
             for (int q = 0; q < 4 && col0 + q < ldo; ++q) store1<WT>(out, ldo, row, col0 + q, w[q], qscale);
+    }
     }
 }
 
@@ -228,7 +233,8 @@ score_fast_kernel(const float* __restrict__ A, int nj, const ColFeat* __restrict
         ColFeat c = live[q] ? cf[col0 + q] : ColFeat{0, 0, 0.0, 0.0};
         j0[q] = c.j0; j1[q] = c.j1; f0[q] = (float)c.wj0; f1[q] = (float)c.wj1;
     }
-    const int64_t row_begin = (int64_t)blockIdx.y * kRowsPerCta;
+    for (int64_t rb = blockIdx.y; rb * kRowsPerCta < n; rb += gridDim.y) {
+    const int64_t row_begin = rb * kRowsPerCta;
     const int64_t row_end = min(n, row_begin + kRowsPerCta);
     for (int64_t row = row_begin; row < row_end; ++row) {
         const float* a = A + row * nj;
@@ -242,6 +248,7 @@ score_fast_kernel(const float* __restrict__ A, int nj, const ColFeat* __restrict
         if (col0 + 4 <= ldo) store4<WT>(out, ldo, row, col0, w, true, qscale);
         else
             for (int q = 0; q < 4 && col0 + q < ldo; ++q) store1<WT>(out, ldo, row, col0 + q, w[q], qscale);
+    }
     }
 }
 
@@ -271,7 +278,8 @@ static int upload_table(mux_ctx_t* ctx, const mux_table_t* tb, DevTable* dt, cud
 template <int WT>
 static void launch_score(int mode, DevTable dt, const RowFeat* rf, const ColFeat* cf, const float* A,
                          int64_t n, int64_t m, void* out, int64_t ldo, double qscale, cudaStream_t st) {
-    dim3 grid((unsigned)((ldo + kColsPerCta - 1) / kColsPerCta), (unsigned)((n + kRowsPerCta - 1) / kRowsPerCta));
+    dim3 grid((unsigned)((ldo + kColsPerCta - 1) / kColsPerCta),
+              (unsigned)std::min<int64_t>((n + kRowsPerCta - 1) / kRowsPerCta, 65535));
     if (mode == MUX_SCORE_EXACT)
         score_exact_kernel<WT><<<grid, kScoreThreads, 0, st>>>(dt, rf, cf, n, m, out, ldo, qscale);
     else

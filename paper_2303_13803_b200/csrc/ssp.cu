@@ -80,8 +80,6 @@ struct Cnt {
     uint32_t errors;
     unsigned long long steps, deep, aborts, augs, xsteps, xdeep, refresh, overflow;
     long long xcyc[4];   // exclusive kernel: pop, horizon re-scans, scan steps, augment
-    int32_t xq, xretry;   // concurrent cluster searches: next deferred row, rows to retry
-    unsigned long long xaborts;
     unsigned long long xpfhits;   // register-key kernel: pops whose row slice was prefetched into smem
 };
 
@@ -855,14 +853,17 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
 }
 
 // ---------------------------------------------------------------------------
-// cluster mode for the long searches: the same dense Dijkstra spread over a
-// thread-block cluster of CL CTAs (CL SMs).  CTA r owns columns
-// [r*mc, (r+1)*mc); prices and column owners are replicated in every CTA's
-// shared memory (constant during a search).  Each step every warp publishes
-// its minimum key in its CTA's slot array, one cluster barrier makes all
-// slots visible, and warp 0 of every CTA reads the CL*32 slots through
-// distributed shared memory (ld.shared::cluster).  Slots are double-buffered
-// by step parity, so a step costs one cluster barrier and one CTA barrier.
+// cluster modes for the long searches: the dense Dijkstra spread over a
+// thread-block cluster of CL CTAs (CL SMs), CTA r owning columns
+// [r*mc, (r+1)*mc).  Two exchanges of the per-step minimum:
+//  * push (ssp_rkey_kernel, m <= CL * 2048): prices and owners are replicated
+//    in every CTA; lanes 0..CL-1 of every warp push the warp's minimum with
+//    st.async into slot [rank*32 + warp] of each CTA, completing bytes on
+//    that CTA's mbarrier; warp 0 of each CTA waits, reduces, re-arms.
+//  * barrier (ssp_slice_kernel, larger m): each CTA keeps only its slice;
+//    warps publish minima in their CTA's slots, one barrier.cluster, warp 0
+//    of every CTA reads the CL*32 slots through DSMEM and fetches the
+//    winner's owner / price from the CTA that holds it.
 // ---------------------------------------------------------------------------
 
 constexpr int CL = 8;
@@ -875,16 +876,14 @@ struct CShared {
     uint64_t bkey[2];        // cluster-wide minimum
     int32_t bown[2];         // its column's owner row (-1 = free column)
     int64_t bprice[2];       // its column's price
-    int32_t qnext;           // concurrent mode: the deferred row this cluster takes next
 };
 
-// Cluster-wide minimum key.  With `fetch`, warp 0 also reads the winning
+// Barrier exchange: cluster-wide minimum key; warp 0 also reads the winning
 // column's owner row and price from the CTA that holds it (DSMEM) before the
 // CTA barrier, so every thread gets them without another round trip.
 template <int CLS>
 __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, int& par, cg::cluster_group& cluster,
-                                                      int32_t mc, int32_t* rocs, int64_t* ps, bool fetch,
-                                                      int32_t& own, int64_t& pw) {
+                                                      int32_t mc, int32_t* rocs, int64_t* ps, int32_t& own, int64_t& pw) {
     v = wmin64(v);
     const int w = threadIdx.x >> 5;
     if (lane_id() == 0) S.slots[par][w] = v;
@@ -900,7 +899,7 @@ __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, in
         x = wmin64(x);
         if (lane_id() == 0) {
             S.bkey[par] = x;
-            if (fetch && x != kNoKey) {
+            if (x != kNoKey) {
                 const int32_t j = (int32_t)(x & 0x7FFFFFu);
                 const int owner = j / mc;
                 S.bown[par] = cluster.map_shared_rank(rocs, owner)[j - owner * mc];
@@ -910,20 +909,16 @@ __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, in
     }
     __syncthreads();
     const uint64_t r = S.bkey[par];
-    if (fetch) { own = S.bown[par]; pw = S.bprice[par]; }
+    own = S.bown[par];
+    pw = S.bprice[par];
     par ^= 1;
     return r;
 }
 
-// Push mode (REPL kernels): no cluster barrier per step.  Lanes 0..CLS-1 of
-// every warp write the warp's minimum straight into slot [rank*32 + warp] of
-// CTA `lane` with st.async, which completes bytes on that CTA's mbarrier; warp
-// 0 of each CTA waits for all CLS*32 minima (one-way DSMEM latency instead of
-// barrier.cluster's all-to-all round trip, its release fence and its L1
-// invalidate), reduces them and re-arms the mbarrier for the buffer's next
-// use.  Buffers alternate by step parity: a CTA can only push step k+2 into a
-// buffer after receiving every CTA's step k+1, which each CTA sends only after
-// it has consumed step k from that buffer.
+// Push exchange buffers: per-warp minima from every CTA, double-buffered by
+// step parity.  A CTA can only push step k+2 into a buffer after receiving
+// every CTA's step k+1, which each CTA sends only after it has consumed step
+// k from that buffer, so no slot is overwritten early.
 template <int CLS>
 struct CPush {
     uint64_t slots[2][CLS * 32];
@@ -949,6 +944,9 @@ __device__ __forceinline__ void cpush_init(CPush<CLS>& P) {
     }
 }
 
+// Push exchange: cluster-wide minimum key.  cand2 (warp 0's lanes): per lane
+// the best key of its slot column other than the winner -- its warp minimum
+// is the runner-up, whose row the caller prefetches.
 template <int CLS, int NW>
 __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPush<CLS>& P, int& par, uint32_t& ph, int rank,
                                                      uint64_t& cand2) {
@@ -982,7 +980,6 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
         }
         const uint64_t xl = x;
         x = wmin64(x);
-        // per lane: the best key other than the winner (its warp-min gives the runner-up pop)
         cand2 = xl == x ? x2 : xl;
         if (ln == 0) {
             S.bkey[par] = x;
@@ -996,132 +993,34 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
     return r;
 }
 
-// Push mode 2: every warp waits on the mbarrier and reduces the CLS*NW
-// minima itself, so a step has no CTA barrier at all.  The mbarrier then
-// counts NW arrivals per phase: each warp arrives (warp 0 with the expected
-// bytes) once it has read the buffer, which arms the buffer's next phase and
-// also certifies that no warp still reads it.
-template <int CLS, int NW>
-__device__ __forceinline__ void cpush_init_all(CPush<CLS>& P) {
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const uint32_t a = smem_u32(&P.bar[b]);
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(NW) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (lane_id() == 0) {
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const uint32_t a = smem_u32(&P.bar[b]);
-            if (threadIdx.x == 0)
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(CLS * NW * 8) : "memory");
-            else
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-        }
-    }
-}
-
-template <int CLS, int NW>
-__device__ __forceinline__ uint64_t cluster_min_push_all(uint64_t v, CPush<CLS>& P, int& par, uint32_t& ph, int rank) {
-    v = wmin64(v);
-    const int w = threadIdx.x >> 5, ln = lane_id();
-    const uint32_t lb = smem_u32(&P.bar[par]);
-    if (ln < CLS) {
-        const uint32_t la = smem_u32(&P.slots[par][rank * 32 + w]);
-        uint32_t ra, rb;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(ln));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(ln));
-        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"(v), "r"(rb)
-                     : "memory");
-    }
-    const uint32_t parity = (ph >> par) & 1u;
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(lb), "r"(parity)
-            : "memory");
-    }
-    uint64_t x = kNoKey;
-#pragma unroll
-    for (int r = 0; r < CLS; ++r) {
-        const uint64_t y = ln < NW ? P.slots[par][r * 32 + ln] : kNoKey;
-        x = y < x ? y : x;
-    }
-    x = wmin64(x);   // warp-synchronous: every lane's reads are done past here
-    if (ln == 0) {
-        if (w == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 8) : "memory");
-        else
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lb) : "memory");
-    }
-    ph ^= 1u << par;
-    par ^= 1;
-    return x;
-}
-
-// REPL: prices and owners of all m columns replicated in every CTA (12 m
-// bytes; no per-step fetch).  Otherwise each CTA keeps only its slice and the
-// winner's owner / price are fetched from its CTA during the reduction.
-template <bool REPL, int CC, int CLS, int NT = CTHREADS>
-__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t conc, int32_t push) {
+// Sliced long-path kernel (m too large to replicate prices and owners in
+// every CTA: the 10k x 40k rounds).  Per local column: distance, price,
+// predecessor, owner, scanned flag in shared memory (25 bytes).
+template <int CC, int CLS>
+__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(CTHREADS, 1)
+ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CShared S;
-    __shared__ __align__(16) CPush<REPL ? CLS : 1> P;
     cg::cluster_group cluster = cg::this_cluster();
+    constexpr int NT = CTHREADS;
     const int32_t m = L.m;
     const int32_t mc = (m + CLS - 1) / CLS;
     const int rank = (int)cluster.block_rank();
     const int32_t c0 = rank * mc;
     const int32_t nloc = max(0, min(mc, m - c0));
-    // REPL: psr[m], rocr[m] replicas first; local slice views ps / rocs point into them
-    int64_t* psr = reinterpret_cast<int64_t*>(smem);
-    int32_t* rocr = reinterpret_cast<int32_t*>(psr + (REPL ? m : 0));
-    int64_t* d = reinterpret_cast<int64_t*>(rocr + (REPL ? ((m + 1) & ~1) : 0));   // [mc] local columns
-    int64_t* ps = REPL ? psr + c0 : d + mc;
-    int32_t* pred = reinterpret_cast<int32_t*>(d + mc + (REPL ? 0 : mc));
-    int32_t* rocs = REPL ? rocr + c0 : pred + mc;
-    uint8_t* fl = reinterpret_cast<uint8_t*>(pred + mc + (REPL ? 0 : mc));       // bit0 scanned
+    int64_t* d = reinterpret_cast<int64_t*>(smem);
+    int64_t* ps = d + mc;
+    int32_t* pred = reinterpret_cast<int32_t*>(ps + mc);
+    int32_t* rocs = pred + mc;
+    uint8_t* fl = reinterpret_cast<uint8_t*>(rocs + mc);       // bit0 scanned
     const int tid = threadIdx.x;
     int par = 0;
     unsigned long long steps = 0;
-    int32_t dummy_own;
-    int64_t dummy_p;
-    uint32_t ph = 0;
-    uint64_t cand2 = kNoKey;
-    if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;   // slots of warps beyond NT/32
+    if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;
     __syncthreads();
-    if (REPL && push) {
-        if ((push & 3) == 2) cpush_init_all<REPL ? CLS : 1, NT / 32>(P);
-        else cpush_init<REPL ? CLS : 1, NT / 32>(P);
-        cluster.sync();
-    }
-    // conc: several clusters take deferred rows from a shared counter; every
-    // popped column is locked (non-blocking CAS) and the tree is validated
-    // against the global state only at augment time, under the locks
-    const int32_t lid = (1 << 30) | (int32_t)(blockIdx.x / CLS);
-    for (int32_t qq = 0;; ++qq) {
-        int32_t q = qq;
-        if (conc) {
-            if (rank == 0 && tid == 0) S.qnext = atomicAdd(&L.cnt->xq, 1);
-            cluster.sync();
-            q = *cluster.map_shared_rank(&S.qnext, 0);
-            cluster.sync();
-        }
-        if (q >= ndef) break;
+    for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
         const int32_t* As = rowp(L, s);
-        if (REPL) {
-            for (int32_t j = tid; j < m; j += NT) {
-                psr[j] = __ldcg(L.p + j);
-                rocr[j] = __ldcg(L.roc + j);
-            }
-            __syncthreads();
-        }
         // one reduction finds both the source's profit (the largest a_sj - p_j)
         // and the first pop (that column, at distance 0; free columns first)
         uint64_t vmin = kNoKey;
@@ -1129,26 +1028,19 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
         for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * NT;
             if (jj < nloc) {
-                int64_t pj;
-                if (REPL) {
-                    pj = ps[jj];
-                } else {
-                    pj = __ldcg(L.p + c0 + jj);
-                    ps[jj] = pj;
-                    rocs[jj] = __ldcg(L.roc + c0 + jj);
-                }
+                const int64_t pj = __ldcg(L.p + c0 + jj);
+                const int32_t r = __ldcg(L.roc + c0 + jj);
+                ps[jj] = pj;
+                rocs[jj] = r;
                 fl[jj] = 0;
                 const int64_t v = pj - (int64_t)__ldg(As + c0 + jj);   // = -(a_sj - p_j)
-                const uint64_t k = ((uint64_t)(v + kDistLim) << 24) | ((REPL ? rocs[jj] : __ldcg(L.roc + c0 + jj)) < 0 ? 0u : (1u << 23)) |
-                                   (uint32_t)(c0 + jj);
+                const uint64_t k = ((uint64_t)(v + kDistLim) << 24) | (r < 0 ? 0u : (1u << 23)) | (uint32_t)(c0 + jj);
                 vmin = k < vmin ? k : vmin;
             }
         }
         int32_t i;
         int64_t pjm;
-        const uint64_t k0 = (REPL && (push & 3) == 2) ? cluster_min_push_all<CLS, NT / 32>(vmin, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
-            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(vmin, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank, cand2)
-                                           : cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
+        const uint64_t k0 = cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, i, pjm);
         const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
         uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
 #pragma unroll
@@ -1159,51 +1051,23 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
                 pred[jj] = s;
             }
         }
-        if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
         bool abandon = false;
-        int32_t pend_jj = -1, pend_old = 0;   // conc: the last CAS, recorded after the next reduction
         while (true) {
             const int32_t jm = (int32_t)(best & 0x7FFFFFu);
             const int64_t dmin = (int64_t)(best >> 24);
-            if (pend_jj >= 0) { fl[pend_jj] |= pend_old == 0 ? 4 : 8; pend_jj = -1; }
-            const bool own_jm = jm >= c0 && jm < c0 + nloc && ((jm - c0) & (NT - 1)) == tid;
-            if (i < 0) {
-                jf = jm;
-                D = dmin;
-                if (conc && own_jm) fl[jm - c0] |= atomicCAS(L.lock + jm, 0, lid) == 0 ? 4 : 8;
-                break;
-            }
+            if (i < 0) { jf = jm; D = dmin; break; }
             // coarse levels: a search past the pop limit is abandoned (row stays free)
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (own_jm) {
-                fl[jm - c0] |= 1;
-                if (conc) { pend_old = atomicCAS(L.lock + jm, 0, lid); pend_jj = jm - c0; }
-            }
+            if (jm >= c0 && jm < c0 + nloc && ((jm - c0) & (NT - 1)) == tid) fl[jm - c0] |= 1;
             const int32_t* Ai = rowp(L, i);
             int32_t av[CC];
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * NT;
                 av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
-            }
-            // runner-up prefetch (push mode, bit 4): while this step's row loads are in
-            // flight, warp 0 pulls this CTA's slice of the row owning the runner-up
-            // column into L2 with one bulk prefetch -- it is often the next pop
-            if (REPL && (push & 4) && tid < 32) {
-                // bit 8: every lane prefetches its own candidate (the best key of its warp
-                // slot over the CLS CTAs, winner excluded) -- up to NW rows per step
-                const uint64_t k2 = (push & 8) ? cand2 : wmin64(cand2);
-                if (k2 != kNoKey && ((push & 8) || tid == 0)) {
-                    const int32_t i2 = rocr[k2 & 0x7FFFFFu];
-                    if (i2 >= 0 && i2 < L.nreal && nloc > 0) {
-                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(L.A + (int64_t)i2 * L.lda + c0) & ~(uintptr_t)15;
-                        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(L.A + (int64_t)i2 * L.lda + c0 + nloc) + 15) & ~(uintptr_t)15;
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
-                    }
-                }
             }
             const int64_t base = dmin + (int64_t)__ldg(Ai + jm) - pjm;
             best = kNoKey;
@@ -1218,39 +1082,8 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
                     best = k < best ? k : best;
                 }
             }
-            best = (REPL && (push & 3) == 2) ? cluster_min_push_all<CLS, NT / 32>(best, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank)
-            : (REPL && push) ? cluster_min_push<CLS, NT / 32>(best, S, *reinterpret_cast<CPush<CLS>*>(&P), par, ph, rank, cand2)
-                                  : cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, !REPL, i, pjm);
-            if (REPL) { i = rocr[best & 0x7FFFFFu]; pjm = psr[best & 0x7FFFFFu]; }
+            best = cluster_min_fetch<CLS>(best, S, par, cluster, mc, rocs, ps, i, pjm);
             ++steps;
-        }
-        if (pend_jj >= 0) { fl[pend_jj] |= pend_old == 0 ? 4 : 8; pend_jj = -1; }
-        if (conc) {
-            // validate the tree under the locks: every scanned column (and the free
-            // end) locked by us, with the price and owner this search started from
-            uint64_t okv = 1;
-#pragma unroll
-            for (int u = 0; u < CC; ++u) {
-                const int32_t jj = tid + u * NT;
-                if (jj < nloc && ((fl[jj] & 1) || c0 + jj == jf)) {
-                    const uint8_t f = fl[jj];
-                    if (!(f & 4) || __ldcg(L.p + c0 + jj) != ps[jj] || __ldcg(L.roc + c0 + jj) != rocs[jj]) okv = 0;
-                }
-            }
-            const bool valid = cluster_min_fetch<CLS>(okv, S, par, cluster, mc, rocs, ps, false, dummy_own, dummy_p) == 1;
-            if (!valid || abandon) {
-#pragma unroll
-                for (int u = 0; u < CC; ++u) {
-                    const int32_t jj = tid + u * NT;
-                    if (jj < nloc && (fl[jj] & 4)) atomicExch(L.lock + c0 + jj, 0);
-                }
-                if (!valid && rank == 0 && tid == 0) {
-                    L.retry[atomicAdd(&L.cnt->xretry, 1)] = s;
-                    atomicAdd(&L.cnt->xaborts, 1ull);
-                }
-                cluster.sync();
-                continue;
-            }
         }
         if (abandon) { cluster.sync(); continue; }
         // dual update on the local scanned columns
@@ -1274,13 +1107,6 @@ __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1) ssp_cluster
         }
         __threadfence();
         cluster.sync();
-        if (conc) {
-#pragma unroll
-            for (int u = 0; u < CC; ++u) {
-                const int32_t jj = tid + u * NT;
-                if (jj < nloc && (fl[jj] & 4)) atomicExch(L.lock + c0 + jj, 0);
-            }
-        }
     }
     if (rank == 0 && tid == 0) atomicAdd(&L.cnt->xsteps, steps);
 }
@@ -1692,15 +1518,16 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     if (n <= 0 || N <= 0) { if (total_q) *total_q = 0; return MUX_OK; }
     if (N > M) { set_error("ssp: needs N <= M"); return MUX_EINVAL; }
     if (n >= (1 << 23)) { set_error("ssp: problem too large"); return MUX_EINVAL; }
-    const bool verbose = getenv("MUX_VERBOSE") != nullptr;
-    const int fct = std::max(2, atoi(getenv("MUX_SSP_F") ? getenv("MUX_SSP_F") : "2"));
-    const int base = std::max(8, atoi(getenv("MUX_SSP_BASE") ? getenv("MUX_SSP_BASE") : "48"));
-    const bool check = getenv("MUX_SSP_CHECK") && *getenv("MUX_SSP_CHECK") == '1';
-    const int32_t serial = getenv("MUX_SSP_SERIAL") && *getenv("MUX_SSP_SERIAL") == '1';
-    const int32_t step_budget = getenv("MUX_SSP_STEPS") ? atoi(getenv("MUX_SSP_STEPS")) : STEP_BUDGET_DEFAULT;
-    const int32_t deep_budget = getenv("MUX_SSP_DEEP") ? atoi(getenv("MUX_SSP_DEEP")) : DEEP_BUDGET_DEFAULT;
+    const Tuning& T = tuning();
+    const bool verbose = T.verbose;
+    const int fct = T.ssp_f;
+    const int base = T.ssp_base;
+    const bool check = T.ssp_check;
+    const int32_t serial = T.ssp_serial ? 1 : 0;
+    const int32_t step_budget = T.ssp_steps;
+    const int32_t deep_budget = T.ssp_deep;
     // pop limit of the long searches at coarse levels (0 = exact coarse levels)
-    const int32_t coarse_pops = getenv("MUX_SSP_COARSE_POPS") ? atoi(getenv("MUX_SSP_COARSE_POPS")) : 0;
+    const int32_t coarse_pops = T.ssp_coarse_pops;
     const bool coarse_exact = coarse_pops == 0;
     auto t0 = std::chrono::steady_clock::now();
 
@@ -1798,48 +1625,29 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_parallel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_exclusive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xsmem));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    // REPL kernels carry the push-exchange buffers (2 * CLS * 32 * 8 B) in static shared memory
-    const size_t push_b8 = sizeof(CPush<CL>), push_b4 = sizeof(CPush<4>), push_b16 = sizeof(CPush<16>);
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b4)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 2, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 8, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    // the register-key kernel carries the push-exchange buffers in static shared memory
+    const size_t push_b8 = sizeof(CPush<CL>);
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<1, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<2, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
-    // threads per CTA of the replicated long-path cluster kernel: 512 (4 columns per
-    // thread) by default -- fewer warps to reduce and to wait for at each pop's CTA
-    // barrier; 256 / 1024 selectable (all cover m <= 16,384)
-    const int cl_nt = getenv("MUX_SSP_CT") ? atoi(getenv("MUX_SSP_CT")) : 512;
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b16)));
-    // per-step exchange of the long-path kernel: st.async + mbarrier push (default) or cluster barrier
-    // 0 = cluster barrier, 1 = push + warp-0 reduction + CTA barrier, 2 = push + every warp reduces
-    // | 4 = runner-up row prefetch into L2 (MUX_SSP_PF, push mode 1 only)
-    const int32_t cpush_mode = getenv("MUX_SSP_PUSH") ? atoi(getenv("MUX_SSP_PUSH")) : 1;
-    // MUX_SSP_PF: 0 off, 1 runner-up row (default), 2 every warp-0 lane's candidate row
-    const int pf_mode = getenv("MUX_SSP_PF") ? atoi(getenv("MUX_SSP_PF")) : 1;
-    const bool cpf = cpush_mode == 1 && pf_mode > 0;
-    const int32_t cpush = cpush_mode | (cpf ? 4 : 0) | (cpf && pf_mode == 2 ? 8 : 0) | (getenv("MUX_SSP_TIME") ? 16 : 0);
-    // long paths on the register-key kernel (MUX_SSP_RKEY=0: the shared-memory kernel)
-    const bool use_rkey = !(getenv("MUX_SSP_RKEY") && *getenv("MUX_SSP_RKEY") == '0');
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<true, 1, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, 4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_cluster_kernel<false, CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    const int cl_size = getenv("MUX_SSP_CL") ? atoi(getenv("MUX_SSP_CL")) : CL;
-    // clusters running long searches concurrently (1 = one at a time)
-    const int32_t conc_clusters = getenv("MUX_SSP_CONC") ? atoi(getenv("MUX_SSP_CONC")) : 1;
-    const bool use_cluster = !(getenv("MUX_SSP_CLUSTER") && *getenv("MUX_SSP_CLUSTER") == '0');
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    // register-key kernel flags: 4 = runner-up row prefetch into shared memory, 16 = per-pop cycle timing
+    const int32_t cpush = (T.ssp_pf ? 4 : 0) | (T.ssp_time ? 16 : 0);
+    const bool use_cluster = T.ssp_cluster;
     int per_sm = 0;
     MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssp_parallel_kernel, PWARPS * 32, psmem));
     if (per_sm < 1) { set_error("ssp kernel cannot be resident"); return MUX_ECUDA; }
     int64_t launches = 0;
     Cnt hc{};
-    cudaEvent_t ev[4];
-    for (auto& e : ev) MUX_CUDA_TRY(cudaEventCreate(&e));
+    // events are destroyed on every exit path
+    struct Events {
+        cudaEvent_t e[4] = {nullptr, nullptr, nullptr, nullptr};
+        ~Events() { for (auto& x : e) if (x) cudaEventDestroy(x); }
+    } evs;
+    cudaEvent_t* ev = evs.e;
+    for (int k = 0; k < 4; ++k) MUX_CUDA_TRY(cudaEventCreate(&ev[k]));
     double ms_dense = 0, ms_par = 0, dense_bytes = 0;
     int64_t dense_searches = 0, dense_launches = 0;
     unsigned long long xsteps_prev = 0;
@@ -1941,63 +1749,20 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const size_t dense_bytes = 21ull * m + 64;
             const int32_t mcl = (m + CL - 1) / CL;
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
-            const size_t clr_bytes = 12ull * m + 8 + 13ull * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
-            const bool repl_ok = use_cluster && m <= CL * CTHREADS * 2 && clr_bytes <= xs_budget - 2048 - push_b8;
-            const bool shard_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
-            // register-key kernel: 12 m replicated + 4 bytes per local column
+            // register-key kernel: 12 m replicated + 4 bytes per local column + two row-slice buffers
             const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * 4 * ((mcl + 8 + 3) & ~3) + 64;
-            const bool rkey_ok = use_rkey && use_cluster && cpush_mode == 1 && mcl <= 512 * 4 &&
-                                 rk_bytes <= xs_budget - 2048 - push_b8;
-            auto launch_cl = [&](int32_t nrows, int32_t conc, int32_t nclusters) {
-                const unsigned g = (unsigned)(CL * nclusters);
-                if (rkey_ok && !conc) {
-                    if (mcl <= 512) ssp_rkey_kernel<1, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
-                    else if (mcl <= 1024) ssp_rkey_kernel<2, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
-                    else if (mcl <= 1536) ssp_rkey_kernel<3, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
-                    else ssp_rkey_kernel<4, CL, 512><<<CL, 512, rk_bytes, st>>>(L, nrows, pl, cpush);
-                } else if (repl_ok) {
-                    if (cl_size == 16 && !conc && 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64 <= xs_budget - 2048 - push_b16)
-                        ssp_cluster_kernel<true, 1, 16><<<16, CTHREADS, 12ull * m + 8 + 13ull * ((m + 15) / 16) + 64, st>>>(L, nrows, pl, 0, cpush);
-                    else if (cl_size == 4 && !conc)
-                        ssp_cluster_kernel<true, 4, 4><<<4, CTHREADS, 12ull * m + 8 + 13ull * ((m + 3) / 4) + 64, st>>>(L, nrows, pl, 0, cpush);
-                    else if (cl_nt == 512 && mcl <= 512)
-                        ssp_cluster_kernel<true, 1, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
-                    else if (cl_nt == 512 && mcl <= 1024)
-                        ssp_cluster_kernel<true, 2, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
-                    else if (cl_nt == 512 && mcl <= 1536)
-                        ssp_cluster_kernel<true, 3, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
-                    else if (cl_nt == 512)
-                        ssp_cluster_kernel<true, 4, CL, 512><<<g, 512, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
-                    else if (cl_nt == 256)
-                        ssp_cluster_kernel<true, 8, CL, 256><<<g, 256, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
-                    else
-                        ssp_cluster_kernel<true, 2, CL><<<g, CTHREADS, clr_bytes, st>>>(L, nrows, pl, conc, cpush);
-                } else if (m <= CL * CTHREADS * 4) {
-                    ssp_cluster_kernel<false, 4, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc, cpush);
-                } else {
-                    ssp_cluster_kernel<false, CCOLS, CL><<<g, CTHREADS, cl_bytes, st>>>(L, nrows, pl, conc, cpush);
-                }
-            };
-            if (repl_ok || shard_ok) {
-                // several long searches at once on separate clusters (locks + validation),
-                // then whatever conflicted on one cluster alone
-                const int32_t ncl = std::min<int32_t>(conc_clusters, ndef_total);
-                if (ncl >= 2) {
-                    L.retry = bufs[0];
-                    MUX_CUDA_TRY(cudaMemsetAsync(&cnt->xq, 0, 2 * sizeof(int32_t), st));
-                    launch_cl(ndef_total, 1, ncl);
-                    int32_t nre = 0;
-                    MUX_CUDA_TRY(cudaMemcpyAsync(&nre, &cnt->xretry, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-                    MUX_CUDA_TRY(cudaStreamSynchronize(st));
-                    if (nre > 0) {
-                        L.defer = bufs[0];
-                        launch_cl(nre, 0, 1);
-                    }
-                } else {
-                    launch_cl(ndef_total, 0, 1);
-                }
-            } else if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && getenv("MUX_SSP_SPARSEX") == nullptr) {
+            const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8;
+            const bool slice_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
+            if (rkey_ok) {
+                if (mcl <= 512) ssp_rkey_kernel<1, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (mcl <= 1024) ssp_rkey_kernel<2, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (mcl <= 1536) ssp_rkey_kernel<3, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                else ssp_rkey_kernel<4, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+            } else if (slice_ok) {
+                if (m <= CL * CTHREADS * 4) ssp_slice_kernel<4, CL><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
+                else ssp_slice_kernel<CCOLS, CL><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
+            } else if (m <= DTHREADS * DCOLS && dense_bytes <= xs_budget - 1024 && !T.ssp_sparsex) {
                 // long searches: dense Dijkstra on one CTA, tables in shared memory
                 ssp_dense_kernel<<<1, DTHREADS, dense_bytes, st>>>(L, ndef_total);
             } else {
@@ -2084,7 +1849,6 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         stats->dense_bytes = dense_bytes;
         stats->dense_launches = dense_launches;
     }
-    for (auto& e : ev) cudaEventDestroy(e);
     if (verbose) fprintf(stderr, "[ssp] n %d levels %d total %.3f ms (host wall), dense %.3f ms, parallel %.3f ms\n", n, nl, ms,
                          ms_dense, ms_par);
     if (cpush & 16) {

@@ -8,6 +8,7 @@ hours, so each case is its own invocation and writes its own fixture):
     python tests/golden/make_large_golden.py q30 10000 40000 0
     python tests/golden/make_large_golden.py f64 4000 4000 0
     python tests/golden/make_large_golden.py q40 4000 4000 0
+    python tests/golden/make_large_golden.py q35 4000 4000 0
 
 Inputs are `paper_2303_13803_b200.synth.make_cluster(n, m, seed)` (the bench's
 snapshot generator; pure numpy) and the default table.  W is the oracle's
@@ -22,8 +23,9 @@ tests/test_oracle_golden.py), with the reference's 1e-6 edge rule
           optimal integer total.  LSA is independent of this repo's solvers; on
           dyadic weights its totals equal the reference's `max_weight_matching`
           (xcheck.py).
-  q40  -- the same with 40-bit int64 weights, solved by the oracle's int64
-          Hungarian (oracle/hungarian.c, restating matching.py:45-101).
+  q35/q40 -- the same with 35- / 40-bit int64 weights, solved by the oracle's
+          int64 Hungarian (oracle/hungarian.c, restating matching.py:45-101);
+          records its assignment and whether the integer optimum is unique.
   f64  -- the reference algorithm itself on the float64 W: the oracle's C
           restatement of `_solve_min_assignment` (bit-identical col_of_row /
           duals to the reference, pinned on golden duals) on the reference's
@@ -78,13 +80,22 @@ def main():
         out.update(qbits=q, solver="scipy.optimize.linear_sum_assignment(maximize=True)",
                    total_q=int(Q[r, c].sum()), total_f64_of_lsa=float(W[r, c].sum()),
                    solve_s=time.time() - t1)
-    elif mode == "q40":
+    elif mode in ("q35", "q36", "q40"):
         from oracle import matching_ref as mr
-        Q = np.rint(W * float(2 ** 40)).astype(np.int64)
+        q = int(mode[1:])
+        Q = np.rint(W * float(2 ** q)).astype(np.int64)
+        nn = max(n, m)
+        P = np.zeros((nn, nn), dtype=np.int64)
+        P[:n, :m] = Q
+        cost = P.max() - P
         t1 = time.time()
-        total, col = mr.max_weight_total_int(Q)
-        out.update(qbits=40, solver="oracle int64 Hungarian (matching.py:45-101 restated)",
-                   total_q=int(total), solve_s=time.time() - t1)
+        col, u, v = mr.solve_min_assignment(cost)
+        solve_s = time.time() - t1
+        total = int(P[np.arange(nn), col].sum())
+        uniq = bool(mr.is_unique_optimum(cost, col, u, v))
+        colr = [int(j) if j < m and Q[i, j] > 0 else -1 for i, j in enumerate(col[:n])]
+        out.update(qbits=q, solver="oracle int64 Hungarian (matching.py:45-101 restated)",
+                   total_q=total, col_of_row=colr, unique_optimum=uniq, solve_s=solve_s)
     elif mode == "f64":
         from oracle import matching_ref as mr
         nn = max(n, m)

@@ -230,6 +230,7 @@ def test_round_total_matches_oracle(cuda, n, m, seed):
 
 def test_global_memory_path(cuda, monkeypatch):
     """The auction path used when prices/rows do not fit shared memory."""
+    monkeypatch.setenv("MUX_TUNING", "1")
     monkeypatch.setenv("MUX_SOLVER", "auction")
     monkeypatch.setenv("MUX_NO_SMEM", "1")
     for n, m, seed in ((300, 300, 7), (150, 420, 8)):
@@ -241,6 +242,7 @@ def test_global_memory_path(cuda, monkeypatch):
 
 def test_tail_thresholds(cuda, monkeypatch):
     """Auction: results stay optimal whatever share of the work the single-CTA tail takes."""
+    monkeypatch.setenv("MUX_TUNING", "1")
     monkeypatch.setenv("MUX_SOLVER", "auction")
     _, Q = _pred_Q(400, 400, 9, 20)
     want, _ = matching_ref.max_weight_total_int(Q)
@@ -329,6 +331,7 @@ def test_golden_pairs_where_optimum_unique(cuda, golden):
 def test_async_tail_forced(cuda, monkeypatch, n, m, seed):
     """The concurrent multi-CTA tail (default for n >= 2048) forced on small
     problems: optimal totals, valid assignment."""
+    monkeypatch.setenv("MUX_TUNING", "1")
     monkeypatch.setenv("MUX_SOLVER", "auction")
     monkeypatch.setenv("MUX_ASYNC_TAIL", "1")
     _, Q = _pred_Q(n, m, seed, 20)

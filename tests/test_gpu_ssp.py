@@ -65,6 +65,12 @@ def certified(monkeypatch):
     monkeypatch.setenv("MUX_SSP_CHECK", "1")
 
 
+@pytest.fixture
+def tuning(monkeypatch):
+    """Experiment knobs are honoured only under MUX_TUNING=1."""
+    monkeypatch.setenv("MUX_TUNING", "1")
+
+
 @pytest.mark.parametrize("n,hi,seed", [(2, 5, 0), (7, 100, 1), (33, 3, 2), (50, 1 << 20, 3), (129, 2, 4),
                                        (300, 1000, 5), (777, 50, 6), (1000, 1 << 30, 7)])
 def test_random_matrices_vs_lsa(cuda, certified, n, hi, seed):
@@ -103,17 +109,18 @@ def test_matches_the_oracle_hungarian(cuda, certified):
         assert total == want
 
 
-def test_auction_and_ssp_agree(cuda, monkeypatch):
+def test_auction_and_ssp_agree(cuda, tuning, monkeypatch):
     """The two GPU solvers (MUX_SOLVER=auction vs the default) reach the same optimum."""
     _, Q = _pred_Q(700, 22, 20)
     _, t_ssp = _match(Q)
+    monkeypatch.setenv("MUX_TUNING", "1")
     monkeypatch.setenv("MUX_SOLVER", "auction")
     _, t_auc = _match(Q)
     assert t_ssp == t_auc == _lsa(Q)
 
 
 @pytest.mark.parametrize("f,base", [("2", "48"), ("4", "48"), ("2", "8"), ("3", "200")])
-def test_level_structure_variants(cuda, certified, monkeypatch, f, base):
+def test_level_structure_variants(cuda, certified, tuning, monkeypatch, f, base):
     """Coarsening factor and base size change only the work, never the optimum."""
     monkeypatch.setenv("MUX_SSP_F", f)
     monkeypatch.setenv("MUX_SSP_BASE", base)
@@ -122,7 +129,7 @@ def test_level_structure_variants(cuda, certified, monkeypatch, f, base):
     assert total == _lsa(Q)
 
 
-def test_long_path_kernels_agree(cuda, certified, monkeypatch):
+def test_long_path_kernels_agree(cuda, certified, tuning, monkeypatch):
     """Cluster (default), single-CTA dense and single-warp sparse long-path modes."""
     cl, Q = _pred_Q(1800, 31, 30)
     want = _lsa(Q)
@@ -133,18 +140,11 @@ def test_long_path_kernels_agree(cuda, certified, monkeypatch):
         assert total == want, env
 
 
-@pytest.mark.parametrize("env", [
-    {"MUX_SSP_PUSH": "0"},                          # barrier.cluster exchange
-    {"MUX_SSP_PUSH": "1", "MUX_SSP_PF": "0"},       # st.async push, no prefetch
-    {"MUX_SSP_PUSH": "2"},                          # push, every warp reduces
-    {"MUX_SSP_CT": "1024"}, {"MUX_SSP_CT": "256"},  # CTA sizes (default 512)
-    {"MUX_SSP_CL": "16"}, {"MUX_SSP_CL": "4"},      # cluster sizes (default 8)
-    {"MUX_SSP_PF": "2"},
-])
-def test_cluster_exchange_variants(cuda, certified, monkeypatch, env):
-    """Per-pop exchange modes and CTA / cluster shapes of the long-path kernel
-    (csrc/ssp.cu ssp_cluster_kernel) give the same optimum; the dual
-    certificate is checked at every level (MUX_SSP_CHECK=1)."""
+@pytest.mark.parametrize("env", [{"MUX_SSP_PF": "0"}, {"MUX_SSP_PF": "1"}])
+def test_long_path_prefetch_variants(cuda, certified, tuning, monkeypatch, env):
+    """The long-path kernel (csrc/ssp.cu ssp_rkey_kernel) with and without the
+    runner-up row prefetch gives the same optimum; the dual certificate is
+    checked at every level (MUX_SSP_CHECK=1)."""
     cl, Q = _pred_Q(2000, 32, 30)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -152,7 +152,7 @@ def test_cluster_exchange_variants(cuda, certified, monkeypatch, env):
     assert total == _lsa(Q), env
 
 
-def test_serial_and_parallel_searches_agree(cuda, certified, monkeypatch):
+def test_serial_and_parallel_searches_agree(cuda, certified, tuning, monkeypatch):
     """Lock-based concurrent warp searches vs one search at a time."""
     cl, Q = _pred_Q(1000, 40, 30)
     _, t_par = _match(Q, keys=(cl.x, cl.y))
@@ -223,6 +223,7 @@ def test_rectangular_sharded_cluster_tables(cuda, certified, monkeypatch):
     t = default_table()
     cl = make_cluster(1200, 20000, seed=5)
     col, total, st = round_arrays(t, cl.x, cl.share, cl.y, qbits=20, stats=True)
+    monkeypatch.setenv("MUX_TUNING", "1")
     monkeypatch.setenv("MUX_SOLVER", "auction")
     _, t_auc = round_arrays(t, cl.x, cl.share, cl.y, qbits=20)
     assert total == t_auc
@@ -251,3 +252,17 @@ def test_more_rows_than_jobs_random(cuda, certified):
     col, total = _match(Q)
     assert total == _lsa(Q)
     _check_assignment(Q, col, total)
+
+
+def test_tuning_knobs_are_gated_and_validated(cuda, monkeypatch):
+    """Experiment knobs only act under MUX_TUNING=1, and an out-of-range value
+    is an error rather than a silent change of the solver."""
+    from paper_2303_13803_b200 import _native as nat
+    cl, Q = _pred_Q(300, 3, 30)
+    want = _lsa(Q)
+    monkeypatch.setenv("MUX_SSP_F", "99")        # stray, ungated: ignored
+    monkeypatch.setenv("MUX_SOLVER", "bogus")
+    assert _match(Q)[1] == want
+    monkeypatch.setenv("MUX_TUNING", "1")        # gated: validated
+    with pytest.raises(nat.NativeError, match="MUX_SSP_F=99"):
+        _match(Q)
