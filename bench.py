@@ -58,6 +58,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-mlp", action="store_true")
+    p.add_argument("--no-schedule", action="store_true")
     return p.parse_args()
 
 
@@ -403,6 +404,27 @@ def run_ours(args, rank, world, local_rank):
                "per_rank": True}
 
     # MLP plugin (tcgen05) scoring of the same N x M pairs: tensor-core roofline
+    # the drop-in call a reference user makes: schedule(records) -> Assignment,
+    # host record handling included (scheduler.py:220-241), at configs 2 and 3
+    sched_line = None
+    if not args.no_schedule and rank == 0:
+        from paper_2303_13803_b200 import SchedulerConfig, schedule
+        from paper_2303_13803_b200.matching import round_qbits
+        from paper_2303_13803_b200.synth import records
+        sched_line = {}
+        for k in (1000, 4000):
+            c = make_cluster(k, k, seed=args.seed)
+            onl, off, states = records(c)
+            schedule(onl, off, states, table, SchedulerConfig(), 900.0)
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                asg = schedule(onl, off, states, table, SchedulerConfig(), 900.0)
+                ts.append((time.perf_counter() - t0) * 1e3)
+            sched_line[f"{k}x{k}"] = {"ms": statistics.median(ts), "pairs": len(asg.pairs),
+                                      "qbits": round_qbits(k),
+                                      "solver": "int64 epsilon-scaling auction" if round_qbits(k) > 30 else "multilevel SSP"}
+
     mlp_line = None
     if not args.no_mlp:
         from paper_2303_13803_b200.mlp import MlpPredictor
@@ -438,7 +460,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, peak_kind = peaks()
-    # dominant kernel: ssp_cluster_kernel (csrc/ssp.cu), the thread-block-cluster
+    # dominant kernel: ssp_rkey_kernel (csrc/ssp.cu), the thread-block-cluster
     # Dijkstra that runs the long augmenting paths of every level.  Algorithmic
     # bytes = one weight row (4*m_level) per pop (SURVEY §8d's per-row-read
     # unit), summed over its pops; time = its CUDA-event duration on the
@@ -480,7 +502,7 @@ def run_ours(args, rank, world, local_rank):
                 "multi_gpu": "each rank solves its own snapshot (seed + rank); value = per-round latency, max over ranks"},
         "replica_rounds_per_s": world / (t_step / 1e3),
         "pair_scores_per_s": n * m / (t_step / 1e3), "parity": parity,
-        "roofline": {"bound": "hbm", "kernel": "ssp_cluster_kernel", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "ssp_rkey_kernel", "achieved": achieved, "peak": hbm,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "traffic_note": f"DRAM read+write bytes per launch (ncu --set full, profiles/{traffic_src})",
                      "algorithmic_bytes": dense_bytes, "kernel_ms": dense_ms,
@@ -494,6 +516,8 @@ def run_ours(args, rank, world, local_rank):
                                      "dual_sweeps")},
         "ms_match": auc_ms, "ms_per_step_all": times,
     }
+    if sched_line is not None:
+        line["schedule_drop_in"] = sched_line
     if mlp_line is not None:
         bf16 = bf16_peak()
         mlp_line.update({"peak_tflops": bf16, "frac": mlp_line["tflops"] / bf16, "bound": "tensor"})

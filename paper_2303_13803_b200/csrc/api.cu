@@ -60,6 +60,7 @@ const Tuning& tuning() {
         t.ssp_pf = knob("MUX_SSP_PF", 1, 0, 1, err) == 1;
         t.ssp_cluster = knob("MUX_SSP_CLUSTER", 1, 0, 1, err) == 1;
         t.ssp_sparsex = knob("MUX_SSP_SPARSEX", 0, 0, 1, err) == 1;
+        t.ssp_one = knob("MUX_SSP_ONE", t.ssp_one, 0, 10240, err);
         t.auc_theta = knob("MUX_THETA", t.auc_theta, 2, 64, err);
         t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 16, err);
         t.auc_k = knob("MUX_K", t.auc_k, 1, 15, err);

@@ -1352,6 +1352,142 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
         for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
 }
 
+// Single-CTA register-key kernel for levels small enough for one SM
+// (m <= 1024 * CC): the same register-resident keys, the whole row slice on
+// one SM, and a block-wide minimum with ONE barrier per pop -- every warp
+// writes its minimum to a parity-double-buffered slot array, and after the
+// barrier every warp reduces the 32 slots itself.  No DSMEM round trip.
+template <int CC>
+__global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
+    constexpr int NT = 1024;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t slots[2][32];
+    const int32_t m = L.m;
+    int64_t* psr = reinterpret_cast<int64_t*>(smem);                          // [m] prices
+    int32_t* rocr = reinterpret_cast<int32_t*>(psr + m);                      // [m] owners
+    int32_t* pred = rocr + ((m + 1) & ~1);                                    // [m] predecessor rows
+    const int tid = threadIdx.x, w = tid >> 5;
+    int par = 0;
+    unsigned long long steps = 0;
+    const bool tm = (flags & 16) != 0;
+    long long tcyc[3] = {0, 0, 0};
+    auto block_min = [&](uint64_t v) -> uint64_t {
+        v = wmin64(v);
+        if (lane_id() == 0) slots[par][w] = v;
+        __syncthreads();
+        const uint64_t x = wmin64(slots[par][lane_id()]);
+        par ^= 1;
+        return x;
+    };
+    for (int32_t q = 0; q < ndef; ++q) {
+        const int32_t s = L.defer[q];
+        const int32_t* As = rowp(L, s);
+        for (int32_t j = tid; j < m; j += NT) {
+            psr[j] = __ldcg(L.p + j);
+            rocr[j] = __ldcg(L.roc + j);
+        }
+        __syncthreads();
+        uint64_t kd[CC], pk[CC];
+        int32_t as[CC];
+        uint64_t vmin = kNoKey;
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t j = tid + u * NT;
+            as[u] = j < m ? __ldg(As + j) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t j = tid + u * NT;
+            if (j < m) {
+                const int64_t pj = psr[j];
+                if (pj < 0 || pj >= kDistLim) atomicOr(&L.cnt->errors, kErrDist);
+                const uint64_t low = (rocr[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                pk[u] = ((uint64_t)pj << 24) | low;
+                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << 24) | low;
+                vmin = k < vmin ? k : vmin;
+                pred[j] = s;
+            } else {
+                pk[u] = kTop;
+            }
+        }
+        const uint64_t k0 = block_min(vmin);
+        const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t j = tid + u * NT;
+            kd[u] = j < m ? (((uint64_t)pis << 24) + pk[u] - ((uint64_t)(uint32_t)as[u] << 24)) : kNoKey;
+        }
+        uint64_t best = k0 & 0xFFFFFFull;
+        int32_t jf;
+        int64_t D;
+        int32_t pops = 0;
+        bool abandon = false;
+        while (true) {
+            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
+            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t i = rocr[jm];
+            if (i < 0) { jf = jm; D = dmin; break; }
+            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            const long long tA = tm ? clock64() : 0;
+            const int32_t* Ai = rowp(L, i);
+            int32_t av[CC];
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t j = tid + u * NT;
+                av[u] = j < m ? __ldg(Ai + j) : 0;
+            }
+            const int64_t aim = (int64_t)__ldg(Ai + jm);
+#pragma unroll
+            for (int u = 0; u < CC; ++u)
+                if (jm == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+            const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << 24;
+            best = kNoKey;
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const uint64_t nk = base + pk[u] - ((uint64_t)(uint32_t)av[u] << 24);
+                if (tid + u * NT < m && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
+                best = kd[u] < best ? kd[u] : best;
+            }
+            const long long tB = tm ? clock64() : 0;
+            best = block_min(best);
+            if (tm) {
+                const long long tC = clock64();
+                tcyc[0] += tB - tA;
+                tcyc[1] += tC - tB;
+                tcyc[2] += 1;
+            }
+            ++steps;
+        }
+        if (!abandon) {
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t j = tid + u * NT;
+                if (j < m && (kd[u] & kTop)) {
+                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> 24), dj = (int64_t)((kd[u] & ~kTop) >> 24);
+                    L.p[j] = pj + (D - dj);
+                }
+            }
+            __syncthreads();   // pred complete
+            if (tid == 0) {
+                int32_t j = jf;
+                while (true) {
+                    const int32_t ii = pred[j];
+                    const int32_t jn = (ii == s) ? -1 : __ldcg(L.cor + ii);
+                    L.roc[j] = ii;
+                    L.cor[ii] = j;
+                    if (ii == s) break;
+                    j = jn;
+                }
+            }
+        }
+        __threadfence();
+        __syncthreads();
+    }
+    if (tid == 0) atomicAdd(&L.cnt->xsteps, steps);
+    if (tm && tid == 0)
+        for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
+}
+
 // ---------------------------------------------------------------------------
 // level setup kernels
 // ---------------------------------------------------------------------------
@@ -1632,6 +1768,12 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     // register-key kernel flags: 4 = runner-up row prefetch into shared memory, 16 = per-pop cycle timing
     const int32_t cpush = (T.ssp_pf ? 4 : 0) | (T.ssp_time ? 16 : 0);
@@ -1754,7 +1896,17 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * 4 * ((mcl + 8 + 3) & ~3) + 64;
             const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8;
             const bool slice_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
-            if (rkey_ok) {
+            // single SM for levels up to T.ssp_one columns: one barrier per pop, no DSMEM
+            const size_t r1_bytes = 16ull * m + 16;
+            const bool rkey1_ok = m <= T.ssp_one && m <= 1024 * 10 && r1_bytes <= xs_budget - 2048;
+            if (rkey1_ok) {
+                if (m <= 1024) ssp_rkey1_kernel<1><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 2048) ssp_rkey1_kernel<2><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 3072) ssp_rkey1_kernel<3><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 5120) ssp_rkey1_kernel<5><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 8192) ssp_rkey1_kernel<8><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else ssp_rkey1_kernel<10><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+            } else if (rkey_ok) {
                 if (mcl <= 512) ssp_rkey_kernel<1, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 1024) ssp_rkey_kernel<2, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 1536) ssp_rkey_kernel<3, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);

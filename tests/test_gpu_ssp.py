@@ -264,5 +264,8 @@ def test_tuning_knobs_are_gated_and_validated(cuda, monkeypatch):
     monkeypatch.setenv("MUX_SOLVER", "bogus")
     assert _match(Q)[1] == want
     monkeypatch.setenv("MUX_TUNING", "1")        # gated: validated
+    with pytest.raises(nat.NativeError, match="MUX_SOLVER=bogus"):
+        _match(Q)
+    monkeypatch.delenv("MUX_SOLVER")
     with pytest.raises(nat.NativeError, match="MUX_SSP_F=99"):
         _match(Q)
