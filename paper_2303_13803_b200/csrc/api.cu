@@ -15,7 +15,8 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
                        cudaStream_t st, int64_t* launches);
 int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
                    int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
-                   int theta, int tail_max, const double* rowkey, const double* colkey);
+                   int theta, int tail_max, const double* rowkey, const double* colkey,
+                   int64_t* price_io = nullptr, int warm = 0);
 
 namespace mux {
 static thread_local std::string g_last_error;
@@ -108,7 +109,7 @@ struct EventPair {
 static int round_device(mux_ctx_t* ctx, const mux_table_t* table, const double* x, const double* s, int64_t n,
                         const double* y, int64_t m, int qbits, void* wq_dev, int64_t ldw, const double* rowkey,
                         const double* colkey, int32_t* col_dev, int64_t* total_q, mux_stats_t* stats,
-                        cudaStream_t st) {
+                        cudaStream_t st, int64_t* price_io = nullptr, int warm = 0) {
     // weights are int32 up to 30 bits, int64 beyond (the exact-parity mode)
     const int wt = qbits > 30 ? MUX_W_I64 : MUX_W_I32;
     const int64_t esz = wt == MUX_W_I64 ? 8 : 4, vec = 16 / esz;
@@ -134,7 +135,7 @@ static int round_device(mux_ctx_t* ctx, const mux_table_t* table, const double* 
     float ms_score = 0.f;
     cudaEventElapsedTime(&ms_score, ev.e[0], ev.e[1]);
     MUX_TRY(mux_match_impl(ctx, W, wt, n, m, ldw, col_dev, total_q, stats, st, tuning().auc_theta,
-                           tuning().auc_tail, rowkey, colkey));
+                           tuning().auc_tail, rowkey, colkey, price_io, warm));
     if (stats) {
         stats->ms_score = ms_score;
         stats->launches += launches;
@@ -346,7 +347,8 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
 
 int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev, const double* share_dev,
                   int64_t n, const double* y_dev, int64_t m, int qbits, void* wq_dev, int64_t ldw,
-                  int32_t* col_of_row_dev, int64_t* total_q, mux_stats_t* stats, void* stream) {
+                  int32_t* col_of_row_dev, int64_t* prices_dev, int warm, int64_t* total_q, mux_stats_t* stats,
+                  void* stream) {
     if (!ctx) { set_error("null context"); return MUX_EINVAL; }
     MUX_TRY(mux_table_validate(table));
     if (n < 0 || m < 0) { set_error("mux_round_dev: bad shape"); return MUX_EINVAL; }
@@ -361,8 +363,9 @@ int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev,
     MUX_CUDA_TRY(cudaMemcpyAsync(rk.data(), x_dev, 8ull * n, cudaMemcpyDeviceToHost, st));
     if (m) MUX_CUDA_TRY(cudaMemcpyAsync(ck.data(), y_dev, 8ull * m, cudaMemcpyDeviceToHost, st));
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    if (warm && !prices_dev) { set_error("mux_round_dev: warm start needs prices_dev"); return MUX_EINVAL; }
     return round_device(ctx, table, x_dev, share_dev, n, y_dev, m, qbits, wq_dev, ldw, rk.data(), ck.data(),
-                        col_of_row_dev, total_q, stats, st);
+                        col_of_row_dev, total_q, stats, st, prices_dev, warm);
 }
 
 }  // extern "C"

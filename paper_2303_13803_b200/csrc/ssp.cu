@@ -1518,6 +1518,22 @@ __global__ void colmax_kernel(const int32_t* A, int64_t lda, int32_t nreal, int3
     p[j] = b;
 }
 
+// warm start: the carried price, or the column maximum for a column the
+// previous round did not have (INT64_MIN).  Any prices are a valid start:
+// each search takes its row's profit as the c-transform max_j (a_ij - p_j).
+__global__ void warm_price_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin, int64_t* p) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int64_t c = pin[j];
+    if (c != INT64_MIN) { p[j] = c; return; }
+    int64_t b = nreal < m ? 0 : INT64_MIN;
+    for (int32_t i = 0; i < nreal && i < m; ++i) {
+        const int64_t v = A[(int64_t)i * lda + j];
+        b = v > b ? v : b;
+    }
+    p[j] = b;
+}
+
 // pi_k of a solved level: a_k,cor(k) - p_cor(k) for matched rows; rows a
 // coarse level left unmatched (its long searches are skipped) take the
 // dual-feasible max_j (a_kj - p_j).  One warp per row.
@@ -1649,7 +1665,7 @@ static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 // zero padding rows (N <= M).
 int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
-                 int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st) {
+                 int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st, const int64_t* price_in) {
     const int32_t n = M;
     if (n <= 0 || N <= 0) { if (total_q) *total_q = 0; return MUX_OK; }
     if (N > M) { set_error("ssp: needs N <= M"); return MUX_EINVAL; }
@@ -1693,7 +1709,8 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     std::vector<LInfo> lv;
     lv.push_back({n, {}, {}, {}});
     std::vector<int32_t> cur_r = ro, cur_c = co;   // sorted original ids of the current level
-    while (lv.back().m > base) {
+    // warm start (price_in: the previous round's optimal column prices): one level
+    while (lv.back().m > base && price_in == nullptr) {
         const int32_t m = lv.back().m;
         std::vector<int32_t> nr, nc, sub;
         for (int32_t k = fct / 2; k < m; k += fct) {
@@ -1828,7 +1845,9 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         int32_t* in0 = reinterpret_cast<int32_t*>(B + o_in[l]);
         init_level_kernel<<<g1, 256, 0, st>>>(m, L.cor, L.roc, L.lock, L.tries, in0, stride);
         // prices
-        if (l == nl - 1) {
+        if (l == nl - 1 && price_in) {
+            warm_price_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, L.nreal, m, price_in, L.p);
+        } else if (l == nl - 1) {
             colmax_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, L.nreal, m, L.p);
         } else {
             const int32_t mc = lv[l + 1].m;

@@ -1,47 +1,36 @@
-"""Config 5 of BASELINE.json: a 100-round trace replay on one B200.
+"""Config-5 replay (BASELINE.json config 5): 100 rounds of the reference's
+gen_trace cluster (10k onlines, offline jobs 0 -> 40k), each a full GPU round,
+cold (multilevel warm start inside each round) and warm (the previous round's
+optimal prices carried across rounds).  Prints one JSON line per mode and
+checks the sampled rounds' totals against the CPU goldens.
 
-10k online workloads whose peak SM activity drifts from round to round (the
-offered share is recomputed with the reference's dynamic_sm formula each
-round), and an offline job set that grows as jobs are submitted: round k
-sees the first min(40000, 400 (k + 1)) jobs (the column set is
-"submitted-by-t", growing to 40k).  Early rounds have fewer jobs than online
-rows (N > M, transposed solve), round 24 is square, later rounds are
-rectangular N < M.  Every round goes through the C ABI `mux_round` with host
-arrays (H2D features, exact scoring, exact matching, canonicalisation, D2H).
-Prints one JSON line with per-round times and totals.
+    python tools/replay.py [rounds] [--check]
 """
-import json, os, sys, time
-import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2303_13803_b200 import default_table
-from paper_2303_13803_b200.scheduler import round_arrays
-from paper_2303_13803_b200.synth import shares_for
+import json
+import os
+import sys
 
-rounds = int(os.environ.get("ROUNDS", "100"))
-N, MMAX, STEP, q = 10000, 40000, 400, int(os.environ.get("QBITS", "30"))
-rng = np.random.default_rng(0)
-base = rng.uniform(0.15, 0.80, N)
-phase = rng.uniform(0, 2 * np.pi, N)
-y_all = rng.uniform(0.60, 0.98, MMAX)
-t = default_table()
-round_arrays(t, base, shares_for(base), y_all, qbits=q)   # warm-up at the largest size (workspace allocations)
-rows = []
-t_all = time.perf_counter()
-for k in range(rounds):
-    x = np.clip(base + 0.05 * np.sin(phase + 0.3 * k), 0.0, 1.0)
-    s = shares_for(x)
-    keep = s > 0
-    xs, ss = x[keep], s[keep]
-    m = min(MMAX, STEP * (k + 1))
-    t0 = time.perf_counter()
-    col, total, st = round_arrays(t, xs, ss, y_all[:m], qbits=q, stats=True)
-    ms = (time.perf_counter() - t0) * 1e3
-    rows.append({"round": k, "n": int(xs.shape[0]), "m": m, "ms": ms, "total_q": total,
-                 "placed": int((col >= 0).sum()), "ms_match": st["ms_match"]})
-    print(f"round {k:3d} n {xs.shape[0]} m {m:5d}: {ms:8.1f} ms  placed {rows[-1]['placed']}", file=sys.stderr, flush=True)
-wall = time.perf_counter() - t_all
-ms_list = [r["ms"] for r in rows]
-print(json.dumps({"config": "100-round replay, 10k online x growing offline set (to 40k), q=%d" % q,
-                  "rounds": rounds, "wall_s": wall, "ms_per_round_mean": float(np.mean(ms_list)),
-                  "ms_per_round_median": float(np.median(ms_list)), "ms_per_round_max": float(np.max(ms_list)),
-                  "per_round": rows}))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_2303_13803_b200 import replay  # noqa: E402
+
+rounds = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 100
+if "--check" in sys.argv:
+    os.environ["MUX_SSP_CHECK"] = "1"
+gold_path = os.path.join(os.path.dirname(replay.FIXTURE), "replay_cfg5_totals.json")
+gold = json.load(open(gold_path))["rounds"] if os.path.exists(gold_path) else {}
+res = {}
+for warm in (False, True):
+    recs = replay.run(rounds=rounds, warm=warm)
+    ms = [r["ms"] for r in recs]
+    checked = {str(r["round"]): r["total_q"] == gold[str(r["round"])]["total_q"] for r in recs if str(r["round"]) in gold}
+    res[warm] = recs
+    print(json.dumps({"mode": "warm" if warm else "cold", "rounds": len(recs), "total_ms": sum(ms),
+                      "mean_ms": sum(ms) / len(ms), "max_ms": max(ms),
+                      "last_round": {k: recs[-1][k] for k in ("n", "m", "ms", "warm")},
+                      "golden_totals_match": checked,
+                      "per_round_ms": [round(x, 2) for x in ms],
+                      "per_round_m": [r["m"] for r in recs],
+                      "dense_pops": [r["stats"]["dense_steps"] for r in recs]}), flush=True)
+same = all(a["total_q"] == b["total_q"] for a, b in zip(res[False], res[True]))
+print(json.dumps({"warm_equals_cold_totals": same}))

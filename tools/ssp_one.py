@@ -22,7 +22,7 @@ for r in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     nat.check(lib.mux_round_dev(ctx, tb, xd.data_ptr(), sd.data_ptr(), n, yd.data_ptr(), n, q, Wq.data_ptr(), ldw,
-                                col.data_ptr(), nat.ctypes.byref(tot), nat.ctypes.byref(st), sp))
+                                col.data_ptr(), None, 0, nat.ctypes.byref(tot), nat.ctypes.byref(st), sp))
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3
     d = st.as_dict()
