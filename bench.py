@@ -343,7 +343,7 @@ def run_ours(args, rank, world, local_rank):
         # the multilevel solve (ordered by the online / offline SM demands), the
         # tie canonicalisation
         nat.check(lib.mux_round_dev(ctx, tb, xd.data_ptr(), sd.data_ptr(), n, yd.data_ptr(), m, q, Wq.data_ptr(), ldw,
-                                    col.data_ptr(), None, 0, nat.ctypes.byref(total), nat.ctypes.byref(st), sptr))
+                                    col.data_ptr(), None, None, 0, nat.ctypes.byref(total), nat.ctypes.byref(st), sptr))
         return st.as_dict(), int(total.value)
 
     for _ in range(args.warmup):

@@ -210,15 +210,18 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table,
  * device, or NULL) receives the optimal column prices in quantised-weight
  * units (INT64_MIN where the solve has none to give: n > m rounds, int64
  * weights).  With warm = 1 it must hold the previous round's prices mapped
- * to this round's columns (INT64_MIN for new columns): the multilevel warm
- * start is then replaced by these prices.  Results are identical either
- * way; only the work changes.
+ * to this round's columns (INT64_MIN for new columns), and warm_col_dev
+ * (int32 [n], device, or NULL) the previous round's column of each row in
+ * this round's indices (-1 = none): previous pairs still tight under the
+ * carried prices are kept and only the other rows are searched, instead of
+ * the multilevel warm start.  Results are identical either way (optimal
+ * total, canonical pairs); only the work changes.
  */
 int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table,
                   const double* x_dev, const double* share_dev, int64_t n,
                   const double* y_dev, int64_t m, int qbits,
                   void* wq_dev, int64_t ldw, int32_t* col_of_row_dev,
-                  int64_t* prices_dev, int warm,
+                  int64_t* prices_dev, const int32_t* warm_col_dev, int warm,
                   int64_t* total_q, mux_stats_t* stats, void* stream);
 
 #ifdef __cplusplus

@@ -91,7 +91,7 @@ def load():
         lib.mux_round.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int, P,
                                   ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         lib.mux_round_dev.argtypes = [P, ctypes.POINTER(MuxTable), P, P, i64, P, i64, ctypes.c_int, P, i64, P,
-                                      P, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
+                                      P, P, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         for name in EXPORTS[2:]:
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib

@@ -16,7 +16,7 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
 int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
                    int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
                    int theta, int tail_max, const double* rowkey, const double* colkey,
-                   int64_t* price_io = nullptr, int warm = 0);
+                   int64_t* price_io = nullptr, int warm = 0, const int32_t* warm_col = nullptr);
 
 namespace mux {
 static thread_local std::string g_last_error;
@@ -62,6 +62,7 @@ const Tuning& tuning() {
         t.ssp_cluster = knob("MUX_SSP_CLUSTER", 1, 0, 1, err) == 1;
         t.ssp_sparsex = knob("MUX_SSP_SPARSEX", 0, 0, 1, err) == 1;
         t.ssp_one = knob("MUX_SSP_ONE", t.ssp_one, 0, 10240, err);
+        t.ssp_rslice = knob("MUX_SSP_RSLICE", 1, 0, 2, err);
         t.auc_theta = knob("MUX_THETA", t.auc_theta, 2, 64, err);
         t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 16, err);
         t.auc_k = knob("MUX_K", t.auc_k, 1, 15, err);
@@ -109,7 +110,8 @@ struct EventPair {
 static int round_device(mux_ctx_t* ctx, const mux_table_t* table, const double* x, const double* s, int64_t n,
                         const double* y, int64_t m, int qbits, void* wq_dev, int64_t ldw, const double* rowkey,
                         const double* colkey, int32_t* col_dev, int64_t* total_q, mux_stats_t* stats,
-                        cudaStream_t st, int64_t* price_io = nullptr, int warm = 0) {
+                        cudaStream_t st, int64_t* price_io = nullptr, int warm = 0,
+                        const int32_t* warm_col = nullptr) {
     // weights are int32 up to 30 bits, int64 beyond (the exact-parity mode)
     const int wt = qbits > 30 ? MUX_W_I64 : MUX_W_I32;
     const int64_t esz = wt == MUX_W_I64 ? 8 : 4, vec = 16 / esz;
@@ -135,7 +137,7 @@ static int round_device(mux_ctx_t* ctx, const mux_table_t* table, const double* 
     float ms_score = 0.f;
     cudaEventElapsedTime(&ms_score, ev.e[0], ev.e[1]);
     MUX_TRY(mux_match_impl(ctx, W, wt, n, m, ldw, col_dev, total_q, stats, st, tuning().auc_theta,
-                           tuning().auc_tail, rowkey, colkey, price_io, warm));
+                           tuning().auc_tail, rowkey, colkey, price_io, warm, warm_col));
     if (stats) {
         stats->ms_score = ms_score;
         stats->launches += launches;
@@ -347,8 +349,8 @@ int mux_round(mux_ctx_t* ctx, const mux_table_t* table, const double* x_host, co
 
 int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev, const double* share_dev,
                   int64_t n, const double* y_dev, int64_t m, int qbits, void* wq_dev, int64_t ldw,
-                  int32_t* col_of_row_dev, int64_t* prices_dev, int warm, int64_t* total_q, mux_stats_t* stats,
-                  void* stream) {
+                  int32_t* col_of_row_dev, int64_t* prices_dev, const int32_t* warm_col_dev, int warm,
+                  int64_t* total_q, mux_stats_t* stats, void* stream) {
     if (!ctx) { set_error("null context"); return MUX_EINVAL; }
     MUX_TRY(mux_table_validate(table));
     if (n < 0 || m < 0) { set_error("mux_round_dev: bad shape"); return MUX_EINVAL; }
@@ -365,7 +367,7 @@ int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev,
     MUX_CUDA_TRY(cudaStreamSynchronize(st));
     if (warm && !prices_dev) { set_error("mux_round_dev: warm start needs prices_dev"); return MUX_EINVAL; }
     return round_device(ctx, table, x_dev, share_dev, n, y_dev, m, qbits, wq_dev, ldw, rk.data(), ck.data(),
-                        col_of_row_dev, total_q, stats, st, prices_dev, warm);
+                        col_of_row_dev, total_q, stats, st, prices_dev, warm, warm_col_dev);
 }
 
 }  // extern "C"

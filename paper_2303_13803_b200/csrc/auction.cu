@@ -1391,7 +1391,7 @@ static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
                  int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st,
-                 const int64_t* price_in = nullptr);
+                 const int64_t* price_in = nullptr, const int32_t* warm_col = nullptr);
 
 __global__ void fill_price_kernel(int64_t* p, int32_t n, int64_t v) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1406,7 +1406,7 @@ __global__ void scale_price_kernel(int64_t* p, int32_t n, int64_t sc) {
 int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t M, int64_t ldw,
                    int32_t* col_out_dev, int64_t* total_q, mux_stats_t* stats, cudaStream_t st,
                    int theta, int tail_max, const double* rowkey, const double* colkey,
-                   int64_t* price_io = nullptr, int warm = 0) {
+                   int64_t* price_io = nullptr, int warm = 0, const int32_t* warm_col = nullptr) {
     if (N < 0 || M < 0 || (N > 0 && ldw < M)) { set_error("mux_match: bad shape"); return MUX_EINVAL; }
     if (wtype != MUX_W_I32 && wtype != MUX_W_I64) { set_error("mux_match: weights must be int32 or int64"); return MUX_EINVAL; }
     const int64_t n = N > M ? N : M;
@@ -1480,7 +1480,8 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             int32_t* owner = reinterpret_cast<int32_t*>(base + o_o);
             int64_t tq = 0;
             MUX_TRY(mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, rowkey, colkey, col_out_dev,
-                                 &tq, price, colr, owner, stats, st, (price_io && warm) ? price_io : nullptr));
+                                 &tq, price, colr, owner, stats, st, (price_io && warm) ? price_io : nullptr,
+                                 (price_io && warm) ? warm_col : nullptr));
             // optimal column prices, in quantised-weight units, for the next round's warm start
             if (price_io) MUX_CUDA_TRY(cudaMemcpyAsync(price_io, price, 8ull * (size_t)M, cudaMemcpyDeviceToDevice, st));
             if (T.canon) {

@@ -81,6 +81,7 @@ struct Cnt {
     unsigned long long steps, deep, aborts, augs, xsteps, xdeep, refresh, overflow;
     long long xcyc[4];   // exclusive kernel: pop, horizon re-scans, scan steps, augment
     unsigned long long xpfhits;   // register-key kernel: pops whose row slice was prefetched into smem
+    unsigned long long xwalk, xwalkcyc, xsearch, xsynccyc;   // timing mode: augmenting-path walk steps / cycles, searches
 };
 
 struct Lvl {
@@ -1352,6 +1353,228 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
         for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
 }
 
+// Register-key kernel for levels too large to replicate prices and owners
+// in every CTA (m > CL * 2048: the 10k x 40k rounds of config 5).  Each
+// thread keeps its columns' keys, prices and owners in registers; a warp's
+// minimum travels with its column's owner row and price packed into a second
+// word (price << 24 | owner + 1), pushed as one 16-byte st.async, so the
+// winner's row and price arrive with the key -- no replicated tables, no
+// DSMEM fetch after the exchange.
+template <int CLS, int NW>
+struct CPush2 {
+    ulonglong2 slots[2][CLS * 32];
+    uint64_t bar[2];
+};
+
+template <int CLS, int NW>
+__device__ __forceinline__ void cpush2_init(CPush2<CLS, NW>& P) {
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&P.bar[b])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&P.bar[b])), "r"(CLS * NW * 16)
+                         : "memory");
+    }
+}
+
+// cluster-wide minimum of (key, payload) pairs by key
+template <int CLS, int NW>
+__device__ __forceinline__ ulonglong2 cluster_min_push2(uint64_t v, uint64_t pay, ulonglong2* bres, CPush2<CLS, NW>& P,
+                                                        int& par, uint32_t& ph, int rank) {
+    const uint64_t wv = wmin64(v);
+    const unsigned who = __ballot_sync(0xffffffffu, v == wv);
+    pay = __shfl_sync(0xffffffffu, pay, __ffs(who) - 1);
+    const int w = threadIdx.x >> 5, ln = lane_id();
+    const uint32_t lb = smem_u32(&P.bar[par]);
+    if (ln < CLS) {
+        const uint32_t la = smem_u32(&P.slots[par][rank * 32 + w]);
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(ln));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(ln));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+                     "l"(wv), "l"(pay), "r"(rb)
+                     : "memory");
+    }
+    if (w == 0) {
+        const uint32_t parity = (ph >> par) & 1u;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(lb), "r"(parity)
+                : "memory");
+        ulonglong2 x = make_ulonglong2(kNoKey, 0ull);
+#pragma unroll
+        for (int r = 0; r < CLS; ++r) {
+            const ulonglong2 y = ln < NW ? P.slots[par][r * 32 + ln] : make_ulonglong2(kNoKey, 0ull);
+            if (y.x < x.x) x = y;
+        }
+        const uint64_t m2 = wmin64(x.x);
+        const unsigned h = __ballot_sync(0xffffffffu, x.x == m2);
+        const uint64_t p2 = __shfl_sync(0xffffffffu, x.y, __ffs(h) - 1);
+        if (ln == 0) {
+            bres[par] = make_ulonglong2(m2, p2);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 16) : "memory");
+        }
+    }
+    ph ^= 1u << par;
+    __syncthreads();
+    const ulonglong2 r = bres[par];
+    par ^= 1;
+    return r;
+}
+
+template <int CC, int CLS, int NT>
+__global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1)
+ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
+    constexpr int NW = NT / 32;
+    unsigned long long walk = 0;
+    long long wcyc = 0, scyc = 0;
+    __shared__ __align__(16) CPush2<CLS, NW> P;
+    __shared__ __align__(16) ulonglong2 bres[2];
+    extern __shared__ __align__(16) unsigned char smem[];
+    int32_t* pred = reinterpret_cast<int32_t*>(smem);   // [mc] predecessor rows (local)
+    cg::cluster_group cluster = cg::this_cluster();
+    const int32_t m = L.m;
+    const int32_t mc = (m + CLS - 1) / CLS;
+    const int rank = (int)cluster.block_rank();
+    const int32_t c0 = rank * mc;
+    const int32_t nloc = max(0, min(mc, m - c0));
+    const int tid = threadIdx.x;
+    int par = 0;
+    uint32_t ph = 0;
+    unsigned long long steps = 0;
+    const bool tm = (flags & 16) != 0;
+    long long tcyc[3] = {0, 0, 0};
+    cpush2_init<CLS, NW>(P);
+    cluster.sync();
+    for (int32_t q = 0; q < ndef; ++q) {
+        const int32_t s = L.defer[q];
+        const int32_t* As = rowp(L, s);
+        uint64_t kd[CC], pk[CC];
+        int32_t own[CC], as[CC];
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * NT;
+            as[u] = jj < nloc ? __ldg(As + c0 + jj) : 0;
+            own[u] = jj < nloc ? __ldcg(L.roc + c0 + jj) : -1;
+        }
+        uint64_t vmin = kNoKey, vpay = 0;
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * NT;
+            if (jj < nloc) {
+                const int32_t j = c0 + jj;
+                const int64_t pj = __ldcg(L.p + j);
+                if (pj < 0 || pj >= kDistLim) atomicOr(&L.cnt->errors, kErrDist);
+                const uint64_t low = (own[u] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
+                pk[u] = ((uint64_t)pj << 24) | low;
+                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << 24) | low;
+                if (k < vmin) { vmin = k; vpay = ((uint64_t)pj << 24) | (uint32_t)(own[u] + 1); }
+                pred[jj] = s;
+            } else {
+                pk[u] = kTop;
+            }
+        }
+        const ulonglong2 r0 = cluster_min_push2<CLS, NW>(vmin, vpay, bres, P, par, ph, rank);
+        const int64_t pis = -((int64_t)(r0.x >> 24) - kDistLim);
+#pragma unroll
+        for (int u = 0; u < CC; ++u) {
+            const int32_t jj = tid + u * NT;
+            kd[u] = jj < nloc ? (((uint64_t)pis << 24) + pk[u] - ((uint64_t)(uint32_t)as[u] << 24)) : kNoKey;
+        }
+        uint64_t best = r0.x & 0xFFFFFFull;
+        uint64_t bpay = r0.y;
+        int32_t jf;
+        int64_t D;
+        int32_t pops = 0;
+        bool abandon = false;
+        while (true) {
+            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
+            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t i = (int32_t)(bpay & 0xFFFFFFu) - 1;
+            const int64_t pjm = (int64_t)(bpay >> 24);
+            if (i < 0) { jf = jm; D = dmin; break; }
+            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            const long long tA = tm ? clock64() : 0;
+            const int32_t* Ai = rowp(L, i);
+            int32_t av[CC];
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t jj = tid + u * NT;
+                av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
+            }
+            const int64_t aim = (int64_t)__ldg(Ai + jm);
+            if (jm >= c0 && jm < c0 + nloc) {
+#pragma unroll
+                for (int u = 0; u < CC; ++u)
+                    if (jm - c0 == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+            }
+            const uint64_t base = (uint64_t)(dmin + aim - pjm) << 24;
+            best = kNoKey;
+            uint64_t pay = 0;
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const uint64_t nk = base + pk[u] - ((uint64_t)(uint32_t)av[u] << 24);
+                if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
+                if (kd[u] < best) { best = kd[u]; pay = ((pk[u] & ~kTop) & ~0xFFFFFFull) | (uint32_t)(own[u] + 1); }
+            }
+            const long long tB = tm ? clock64() : 0;
+            const ulonglong2 r = cluster_min_push2<CLS, NW>(best, pay, bres, P, par, ph, rank);
+            best = r.x;
+            bpay = r.y;
+            if (tm) {
+                const long long tC = clock64();
+                tcyc[0] += tB - tA;
+                tcyc[1] += tC - tB;
+                tcyc[2] += 1;
+            }
+            ++steps;
+        }
+        if (!abandon) {
+#pragma unroll
+            for (int u = 0; u < CC; ++u) {
+                const int32_t jj = tid + u * NT;
+                if (jj < nloc && (kd[u] & kTop)) {
+                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> 24), dj = (int64_t)((kd[u] & ~kTop) >> 24);
+                    L.p[c0 + jj] = pj + (D - dj);
+                }
+            }
+            if (rank == 0 && tid == 0) {
+                const long long tw = tm ? clock64() : 0;
+                int32_t j = jf;
+                while (true) {
+                    const int owner = j / mc;
+                    const int32_t ii = cluster.map_shared_rank(pred, owner)[j - owner * mc];
+                    const int32_t jn = (ii == s) ? -1 : __ldcg(L.cor + ii);
+                    L.roc[j] = ii;
+                    L.cor[ii] = j;
+                    ++walk;
+                    if (ii == s) break;
+                    j = jn;
+                }
+                if (tm) wcyc += clock64() - tw;
+            }
+        }
+        const long long ts = tm ? clock64() : 0;
+        __threadfence();
+        cluster.sync();
+        if (tm) scyc += clock64() - ts;
+    }
+    if (rank == 0 && tid == 0) atomicAdd(&L.cnt->xsteps, steps);
+    if (tm && rank == 0 && tid == 0) {
+        for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
+        atomicAdd(&L.cnt->xwalk, walk);
+        atomicAdd(&L.cnt->xwalkcyc, (unsigned long long)wcyc);
+        atomicAdd(&L.cnt->xsearch, (unsigned long long)ndef);
+        atomicAdd(&L.cnt->xsynccyc, (unsigned long long)scyc);
+    }
+}
+
 // Single-CTA register-key kernel for levels small enough for one SM
 // (m <= 1024 * CC): the same register-resident keys, the whole row slice on
 // one SM, and a block-wide minimum with ONE barrier per pop -- every warp
@@ -1518,20 +1741,96 @@ __global__ void colmax_kernel(const int32_t* A, int64_t lda, int32_t nreal, int3
     p[j] = b;
 }
 
-// warm start: the carried price, or the column maximum for a column the
-// previous round did not have (INT64_MIN).  Any prices are a valid start:
-// each search takes its row's profit as the c-transform max_j (a_ij - p_j).
-__global__ void warm_price_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin, int64_t* p) {
+// ---------------------------------------------------------------------------
+// warm start across rounds (config-5 replays): the previous round's optimal
+// column prices (INT64_MIN = a column it did not have) and its assignment
+// mapped to this round's indices.  Any prices with row profits taken as the
+// c-transform pi_i = max_j (a_ij - p_j) are dual feasible; every previous
+// pair that is still tight under them stays matched, and only the rest of
+// the rows (those whose features changed, new columns' takers) are searched.
+//  1. pi_i over the carried columns (warp per real row)
+//  2. new columns priced at max(max_i (a_ij - pi_i), p_min): feasible for
+//     every real row and for the zero padding rows (pi_pad = -p_min)
+//  3. tight previous pairs kept; padding rows take free columns at p_min
+// ---------------------------------------------------------------------------
+
+// block-wide minimum of the carried prices into *pmin (pre-set to INT64_MAX)
+__global__ void warm_pmin_kernel(const int64_t* pin, int32_t m, unsigned long long* pmin) {
+    int64_t b = INT64_MAX;
+    for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x)
+        if (pin[j] != INT64_MIN) b = pin[j] < b ? pin[j] : b;
+    b = wmin64s(b);
+    if (lane_id() == 0 && b != INT64_MAX) atomicMin(reinterpret_cast<long long*>(pmin), (long long)b);
+}
+
+__global__ void warm_profit_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin,
+                                   int64_t* pi) {
+    const int32_t k = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (k >= nreal) return;
+    int64_t b = -kInf;
+    for (int32_t c = lane_id(); c < m; c += 32) {
+        const int64_t pc = pin[c];
+        if (pc != INT64_MIN) {
+            const int64_t v = (int64_t)A[(int64_t)k * lda + c] - pc;
+            b = v > b ? v : b;
+        }
+    }
+    b = wmax64s(b);
+    if (lane_id() == 0) pi[k] = b;
+}
+
+__global__ void warm_price_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin,
+                                  const int64_t* pi, const unsigned long long* pminp, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     const int64_t c = pin[j];
     if (c != INT64_MIN) { p[j] = c; return; }
-    int64_t b = nreal < m ? 0 : INT64_MIN;
-    for (int32_t i = 0; i < nreal && i < m; ++i) {
-        const int64_t v = A[(int64_t)i * lda + j];
+    int64_t b = nreal < m ? (int64_t)*pminp : INT64_MIN;   // padding rows: 0 - pi_pad = p_min
+    for (int32_t i = 0; i < nreal; ++i) {
+        const int64_t v = (int64_t)A[(int64_t)i * lda + j] - pi[i];
         b = v > b ? v : b;
     }
     p[j] = b;
+}
+
+// keep the previous pairs that are still tight; the unmatched rows form the
+// search list (cnt->qhead counts them)
+__global__ void warm_match_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int32_t* wcol,
+                                  const int64_t* pi, const int64_t* p, int32_t* cor, int32_t* roc) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nreal) return;
+    const int32_t c = wcol ? wcol[i] : -1;
+    if (c >= 0 && c < m && (int64_t)A[(int64_t)i * lda + c] - p[c] == pi[i]) {
+        cor[i] = c;
+        roc[c] = i;
+    }
+}
+
+// padding rows [plo, phi) take the free columns priced p_min (tight for them:
+// their profit is -p_min); padding rows are interchangeable
+__global__ void warm_pad_kernel(int32_t plo, int32_t phi, int32_t m, const int64_t* p, const unsigned long long* pminp,
+                                int32_t* cor, int32_t* roc, int32_t* counter) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m || roc[j] >= 0 || p[j] != (int64_t)*pminp) return;
+    const int32_t k = atomicAdd(counter, 1);
+    if (plo + k < phi) {
+        roc[j] = plo + k;
+        cor[plo + k] = j;
+    }
+}
+
+// unmatched rows among [lo, hi) -> in[]
+__global__ void warm_list_kernel(int32_t lo, int32_t hi, const int32_t* cor, int32_t* in, int32_t* counter) {
+    const int32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < hi && cor[i] < 0) in[atomicAdd(counter, 1)] = i;
+}
+
+// split a row list into real rows and padding rows [plo, phi)
+__global__ void split_rows_kernel(int32_t n, const int32_t* in, int32_t plo, int32_t phi, int32_t* real, int32_t* counter) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int32_t r = in[k];
+    if (r < plo || r >= phi) real[atomicAdd(counter, 1)] = r;
 }
 
 // pi_k of a solved level: a_k,cor(k) - p_cor(k) for matched rows; rows a
@@ -1665,7 +1964,8 @@ static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 // zero padding rows (N <= M).
 int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
-                 int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st, const int64_t* price_in) {
+                 int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st, const int64_t* price_in,
+                 const int32_t* warm_col) {
     const int32_t n = M;
     if (n <= 0 || N <= 0) { if (total_q) *total_q = 0; return MUX_OK; }
     if (N > M) { set_error("ssp: needs N <= M"); return MUX_EINVAL; }
@@ -1705,7 +2005,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     std::stable_sort(co.begin(), co.end(), [&](int32_t a, int32_t b) { return ck[a] < ck[b]; });
 
     // level hierarchy: level 0 = all (original order); level l+1 = every f-th of level l's sorted order
-    struct LInfo { int32_t m; std::vector<int32_t> rows, cols, sub; };
+    struct LInfo { int32_t m; std::vector<int32_t> rows, cols, sub; int32_t plo = 0, phi = 0; };
     std::vector<LInfo> lv;
     lv.push_back({n, {}, {}, {}});
     std::vector<int32_t> cur_r = ro, cur_c = co;   // sorted original ids of the current level
@@ -1729,6 +2029,16 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         cur_c = nc;
     }
     const int nl = (int)lv.size();
+    // padding rows of each level (the reference's zero rows when N < M): the
+    // original rows N..M-1 at level 0; at coarse levels they sort first
+    for (int l = 0; l < nl; ++l) {
+        if (N >= M) continue;
+        if (l == 0) { lv[l].plo = N; lv[l].phi = M; continue; }
+        int32_t np = 0;
+        for (int32_t r : lv[l].rows) np += r >= N;
+        lv[l].plo = 0;
+        lv[l].phi = np;
+    }
 
     // workspace
     size_t off = 0;
@@ -1737,7 +2047,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     const size_t o_tot = take(32);
     const size_t o_zero = take(4ull * n + 64);
     std::vector<size_t> o_A(nl), o_p(nl), o_cor(nl), o_roc(nl), o_lock(nl), o_cj(nl), o_ca(nl), o_tau(nl), o_in(nl),
-        o_re(nl), o_de(nl), o_tr(nl), o_pi(nl), o_sub(nl), o_rows(nl), o_cols(nl);
+        o_re(nl), o_de(nl), o_tr(nl), o_pi(nl), o_sub(nl), o_rows(nl), o_cols(nl), o_rl(nl);
     for (int l = 0; l < nl; ++l) {
         const size_t m = (size_t)lv[l].m;
         o_A[l] = l ? take(4 * m * m) : 0;
@@ -1747,6 +2057,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         o_pi[l] = take(8 * m);
         o_sub[l] = take(4 * (lv[l].sub.size() + 1));
         o_rows[l] = take(4 * m); o_cols[l] = take(4 * m);
+        o_rl[l] = take(4 * m + 64);
     }
     const size_t o_xd = take(8ull * n), o_xp = take(4ull * n), o_xs = take(4ull * n), o_xc = take(4ull * n + 256),
                  o_xh = take(4ull * n);
@@ -1785,6 +2096,10 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<16, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
@@ -1844,9 +2159,26 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         const unsigned g1 = (unsigned)((m + 255) / 256);
         int32_t* in0 = reinterpret_cast<int32_t*>(B + o_in[l]);
         init_level_kernel<<<g1, 256, 0, st>>>(m, L.cor, L.roc, L.lock, L.tries, in0, stride);
+        int32_t nwarm = m;   // rows to search (warm start: the unmatched ones)
         // prices
         if (l == nl - 1 && price_in) {
-            warm_price_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, L.nreal, m, price_in, L.p);
+            int64_t* pi = reinterpret_cast<int64_t*>(B + o_pi[l]);
+            unsigned long long* pmin = reinterpret_cast<unsigned long long*>(B + o_tot);
+            int32_t* wcount = reinterpret_cast<int32_t*>(B + o_tot + 8);
+            const unsigned long long big = (unsigned long long)INT64_MAX;
+            MUX_CUDA_TRY(cudaMemcpyAsync(pmin, &big, 8, cudaMemcpyHostToDevice, st));
+            MUX_CUDA_TRY(cudaMemsetAsync(wcount, 0, 8, st));
+            warm_pmin_kernel<<<std::min<unsigned>(g1, 256u), 256, 0, st>>>(price_in, m, pmin);
+            warm_profit_kernel<<<(unsigned)(((int64_t)L.nreal * 32 + 255) / 256), 256, 0, st>>>(L.A, L.lda, L.nreal, m,
+                                                                                              price_in, pi);
+            warm_price_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, L.nreal, m, price_in, pi, pmin, L.p);
+            warm_match_kernel<<<(unsigned)((L.nreal + 255) / 256), 256, 0, st>>>(L.A, L.lda, L.nreal, m, warm_col, pi,
+                                                                                  L.p, L.cor, L.roc);
+            if (L.nreal < m) warm_pad_kernel<<<g1, 256, 0, st>>>(L.nreal, m, m, L.p, pmin, L.cor, L.roc, wcount);
+            warm_list_kernel<<<g1, 256, 0, st>>>(0, m, L.cor, in0, wcount + 1);
+            MUX_CUDA_TRY(cudaMemcpyAsync(&nwarm, wcount + 1, 4, cudaMemcpyDeviceToHost, st));
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            launches += 6;
         } else if (l == nl - 1) {
             colmax_kernel<<<g1, 256, 0, st>>>(L.A, L.lda, L.nreal, m, L.p);
         } else {
@@ -1869,12 +2201,14 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             MUX_CUDA_TRY(cudaStreamSynchronize(st));
             ms_setup = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
         }
-        // parallel passes
-        const int32_t* list = in0;
-        int32_t nlist = m;
+        // parallel passes over a row list, then the long paths of the deferred rows
         int32_t* bufs[2] = {L.retry, reinterpret_cast<int32_t*>(B + o_pi[l])};   // pi scratch doubles as 2nd retry list
+        int32_t ndef_level = 0, passes_level = 0;
+        double ms_par_wall = 0;
+        auto solve_rows = [&](const int32_t* list, int32_t nlist) -> int {
         int pass = 0;
         int32_t ndef_total = 0;
+        const auto tl2 = std::chrono::steady_clock::now();
         MUX_CUDA_TRY(cudaEventRecord(ev[0], st));
         while (nlist > 0) {
             L.in = list;
@@ -1901,7 +2235,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             if (pass > 256) { set_error("ssp: retry passes exceeded"); return MUX_ELIMIT; }
         }
         MUX_CUDA_TRY(cudaEventRecord(ev[1], st));
-        const double ms_par_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
+        ms_par_wall += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl2).count();
         MUX_CUDA_TRY(cudaEventRecord(ev[2], st));
         // coarse levels only supply warm duals: their long searches are skipped
         // (the partial assignment with its duals is feasible and near-optimal)
@@ -1913,7 +2247,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const int32_t pl = l == 0 ? 0 : coarse_pops;
             // register-key kernel: 12 m replicated + 4 bytes per local column + two row-slice buffers
             const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * 4 * ((mcl + 8 + 3) & ~3) + 64;
-            const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8;
+            const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8 && T.ssp_rslice != 2;
             const bool slice_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
             // single SM for levels up to T.ssp_one columns: one barrier per pop, no DSMEM
             const size_t r1_bytes = 16ull * m + 16;
@@ -1930,6 +2264,13 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
                 else if (mcl <= 1024) ssp_rkey_kernel<2, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 1536) ssp_rkey_kernel<3, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else ssp_rkey_kernel<4, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+            } else if (use_cluster && T.ssp_rslice > 0 && mcl <= 512 * 16) {
+                // register keys with (key, owner | price) pushes: no replicated tables
+                const size_t rs_bytes = 4ull * mcl + 64;
+                if (mcl <= 512 * 3) ssp_rkey_slice_kernel<3, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (mcl <= 512 * 6) ssp_rkey_slice_kernel<6, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (mcl <= 512 * 10) ssp_rkey_slice_kernel<10, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
+                else ssp_rkey_slice_kernel<16, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
             } else if (slice_ok) {
                 if (m <= CL * CTHREADS * 4) ssp_slice_kernel<4, CL><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
                 else ssp_slice_kernel<CCOLS, CL><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
@@ -1960,6 +2301,41 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             dense_searches += ndef_total;
             dense_launches += ndef_total > 0 ? 1 : 0;
         }
+        ndef_level += ndef_total;
+        passes_level += pass;
+        return MUX_OK;
+        };
+        const int32_t plo = lv[l].plo, phi = lv[l].phi;
+        if (phi <= plo || price_in) {
+            MUX_TRY(solve_rows(in0, nwarm));
+        } else {
+            // real rows first (their searches never meet padding rows, which are
+            // all still free), then the interchangeable padding rows: in bulk on
+            // the free columns at the minimum price (tight for them), the rest
+            // by search.  Row order never changes the optimum.
+            int32_t* real = reinterpret_cast<int32_t*>(B + o_rl[l]);
+            int32_t* cnts = reinterpret_cast<int32_t*>(B + o_tot + 8);
+            unsigned long long* pmin = reinterpret_cast<unsigned long long*>(B + o_tot);
+            MUX_CUDA_TRY(cudaMemsetAsync(cnts, 0, 16, st));
+            split_rows_kernel<<<g1, 256, 0, st>>>(m, in0, plo, phi, real, cnts);
+            int32_t nr = 0;
+            MUX_CUDA_TRY(cudaMemcpyAsync(&nr, cnts, 4, cudaMemcpyDeviceToHost, st));
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            MUX_TRY(solve_rows(real, nr));
+            const unsigned long long big = (unsigned long long)INT64_MAX;
+            MUX_CUDA_TRY(cudaMemcpyAsync(pmin, &big, 8, cudaMemcpyHostToDevice, st));
+            warm_pmin_kernel<<<std::min<unsigned>(g1, 256u), 256, 0, st>>>(L.p, m, pmin);
+            warm_pad_kernel<<<g1, 256, 0, st>>>(plo, phi, m, L.p, pmin, L.cor, L.roc, cnts + 1);
+            warm_list_kernel<<<(unsigned)((phi - plo + 255) / 256), 256, 0, st>>>(plo, phi, L.cor, real, cnts + 2);
+            int32_t np = 0;
+            MUX_CUDA_TRY(cudaMemcpyAsync(&np, cnts + 2, 4, cudaMemcpyDeviceToHost, st));
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            launches += 4;
+            if (np > 0) MUX_TRY(solve_rows(real, np));
+        }
+        const int32_t ndef_total = ndef_level;
+        const int pass = passes_level;
+
         if (hc.errors) {
             set_error(std::string("ssp: device error flags ") + std::to_string(hc.errors));
             return MUX_ELIMIT;
@@ -2024,8 +2400,11 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
                          ms_dense, ms_par);
     if (cpush & 16) {
         const double k = hc.xcyc[2] > 0 ? (double)hc.xcyc[2] : 1.0;
-        fprintf(stderr, "[ssp-time] pops %lld cycles/pop (CTA 0 warp 0): load+relax %.0f exchange %.0f | prefetch hits %.3f\n",
-                (long long)hc.xcyc[2], hc.xcyc[0] / k, hc.xcyc[1] / k, (double)hc.xpfhits / (double)std::max(1ull, hc.xsteps));
+        fprintf(stderr, "[ssp-time] pops %lld cycles/pop (CTA 0 warp 0): load+relax %.0f exchange %.0f | prefetch hits %.3f"
+                        " | searches %llu walk steps %llu (%.0f cycles each) end-of-search sync %.0f cycles each\n",
+                (long long)hc.xcyc[2], hc.xcyc[0] / k, hc.xcyc[1] / k, (double)hc.xpfhits / (double)std::max(1ull, hc.xsteps),
+                hc.xsearch, hc.xwalk, (double)hc.xwalkcyc / (double)std::max(1ull, hc.xwalk),
+                (double)hc.xsynccyc / (double)std::max(1ull, hc.xsearch));
     }
     return MUX_OK;
 }

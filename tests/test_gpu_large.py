@@ -56,7 +56,7 @@ def _round(torch, n, m, seed, qbits, wq=True):
     col = torch.empty(n, dtype=torch.int32, device=dev)
     tot, st = nat.ctypes.c_int64(0), nat.MuxStats()
     nat.check(nat.load().mux_round_dev(nat.context(0), tb, xd.data_ptr(), sd.data_ptr(), n, yd.data_ptr(), m, qbits,
-                                       W.data_ptr(), ldw, col.data_ptr(), None, 0, nat.ctypes.byref(tot), nat.ctypes.byref(st),
+                                       W.data_ptr(), ldw, col.data_ptr(), None, None, 0, nat.ctypes.byref(tot), nat.ctypes.byref(st),
                                        nat.stream_ptr()))
     torch.cuda.synchronize()
     del keep

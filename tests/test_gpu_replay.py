@@ -16,7 +16,7 @@ GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "repla
 def test_replay_rounds_cold_and_warm(cuda, monkeypatch):
     from paper_2303_13803_b200 import replay
     monkeypatch.setenv("MUX_SSP_CHECK", "1")
-    k = 16   # rounds 0-11 have fewer jobs than onlines (transposed solve), 12+ more
+    k = 15   # rounds 0-11 have fewer jobs than onlines (transposed solve), 12+ more; 13-14 warm
     cold = replay.run(rounds=k, warm=False)
     warm = replay.run(rounds=k, warm=True)
     assert [r["total_q"] for r in cold] == [r["total_q"] for r in warm]
