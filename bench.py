@@ -454,8 +454,11 @@ def run_ours(args, rank, world, local_rank):
             ts.append(e0.elapsed_time(e1))
         mlp_ms = sorted(ts)[len(ts) // 2]
         flops = 2.0 * 64 * 64 * 2 * n * m + 4.0 * 64 * n * m
+        issued = 2.0 * 2 * 144 * 64 * n * m          # tensor flops issued: K = 64 hi + 64 lo + 16 bias per layer
         mlp_line = {"ms": mlp_ms, "tflops": flops / (mlp_ms / 1e3) / 1e12, "flops": flops,
-                    "note": "layers 2-3 as tcgen05 kind::f16 M128xN64xK16, fp32 TMEM accumulate"}
+                    "tensor_tflops_issued": issued / (mlp_ms / 1e3) / 1e12,
+                    "note": "algorithmic flops (16.6 kFLOP/pair); layers 2-3 as tcgen05 kind::f16 M128 N64, "
+                            "split fp16 activations (hi + lo) + bias column: K = 144, fp32 TMEM accumulate"}
 
     if rank != 0:
         return
@@ -520,7 +523,8 @@ def run_ours(args, rank, world, local_rank):
         line["schedule_drop_in"] = sched_line
     if mlp_line is not None:
         bf16 = bf16_peak()
-        mlp_line.update({"peak_tflops": bf16, "frac": mlp_line["tflops"] / bf16, "bound": "tensor"})
+        mlp_line.update({"peak_tflops": bf16, "frac": mlp_line["tflops"] / bf16, "bound": "tensor",
+                         "tensor_frac_issued": mlp_line["tensor_tflops_issued"] / bf16})
         line["mlp_plugin"] = mlp_line
     print(json.dumps(line), flush=True)
 

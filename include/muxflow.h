@@ -143,8 +143,9 @@ int mux_score_table(mux_ctx_t* ctx, const mux_table_t* table,
 
 /*
  * MLP pair scoring: the batched N x M evaluation of the MLP plugin, layers
- * 2-3 as tcgen05 bf16 GEMMs with fp32 TMEM accumulation and fused
- * bias/ReLU/dot epilogues.  on_dev: float64 [n][4], share_dev: float64 [n],
+ * 2-3 as tcgen05 fp16 GEMMs over split (hi + lo) activations with fp32 TMEM
+ * accumulation and fused ReLU/dot epilogues; W2, b2, W3, b3 must be fp16
+ * values (MUX_EINVAL otherwise).  on_dev: float64 [n][4], share_dev: float64 [n],
  * off_dev: float64 [m][4] (DEVICE).  out_dev: [n][ldo] of MUX_W_F32 (scores)
  * or MUX_W_I32 (rint(w * 2^qbits) after the 1e-6 edge floor), ldo % 4 == 0.
  */
@@ -223,6 +224,20 @@ int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table,
                   void* wq_dev, int64_t ldw, int32_t* col_of_row_dev,
                   int64_t* prices_dev, const int32_t* warm_col_dev, int warm,
                   int64_t* total_q, mux_stats_t* stats, void* stream);
+
+/*
+ * One scheduling round with the MLP plugin as the predictor, from HOST
+ * feature arrays: on_host [n][4] and off_host [m][4] (gpu_utilization,
+ * sm_activity, sm_occupancy, iter_time_separate), share_host [n].  H2D,
+ * MLP scores of every pair quantised to rint(w * 2^qbits) (qbits <= 30, the
+ * 1e-6 edge floor first), the exact matching with its tie
+ * canonicalisation, D2H of col_of_row (-1 = unmatched).
+ */
+int mux_round_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp,
+                  const double* on_host, const double* share_host, int64_t n,
+                  const double* off_host, int64_t m, int qbits,
+                  int32_t* col_of_row_host, int64_t* total_q,
+                  mux_stats_t* stats, void* stream);
 
 #ifdef __cplusplus
 }

@@ -370,4 +370,51 @@ int mux_round_dev(mux_ctx_t* ctx, const mux_table_t* table, const double* x_dev,
                         col_of_row_dev, total_q, stats, st, prices_dev, warm, warm_col_dev);
 }
 
+int mux_round_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp, const double* on_host, const double* share_host, int64_t n,
+                  const double* off_host, int64_t m, int qbits, int32_t* col_of_row_host, int64_t* total_q,
+                  mux_stats_t* stats, void* stream) {
+    if (!ctx || !mlp) { set_error("null argument"); return MUX_EINVAL; }
+    if (n < 0 || m < 0) { set_error("mux_round_mlp: bad shape"); return MUX_EINVAL; }
+    if (qbits < 1 || qbits > 30) { set_error("mux_round_mlp: qbits must be in [1, 30]"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (total_q) *total_q = 0;
+    if (n == 0) return MUX_OK;
+    const size_t fbytes = sizeof(double) * (size_t)(5 * n + 4 * m);
+    MUX_TRY(pinned_ensure(ctx, fbytes));
+    double* hp = static_cast<double*>(ctx->pinned);
+    memcpy(hp, on_host, sizeof(double) * 4 * n);
+    memcpy(hp + 4 * n, share_host, sizeof(double) * n);
+    if (m) memcpy(hp + 5 * n, off_host, sizeof(double) * 4 * m);
+    MUX_TRY(ctx->feat_in.ensure(fbytes));
+    double* df = ctx->feat_in.as<double>();
+    MUX_CUDA_TRY(cudaMemcpyAsync(df, hp, fbytes, cudaMemcpyHostToDevice, st));
+    const int64_t ldw = ((m + 3) / 4) * 4;
+    MUX_TRY(ctx->wq.ensure(4ull * (size_t)n * (size_t)(ldw > 0 ? ldw : 4)));
+    MUX_TRY(ctx->colout.ensure(sizeof(int32_t) * (size_t)n));
+    int32_t* col_dev = ctx->colout.as<int32_t>();
+    EventPair ev;
+    MUX_CUDA_TRY(cudaEventCreate(&ev.e[0]));
+    MUX_CUDA_TRY(cudaEventCreate(&ev.e[1]));
+    MUX_CUDA_TRY(cudaEventRecord(ev.e[0], st));
+    int64_t launches = 0;
+    if (m > 0)
+        MUX_TRY(mux_score_mlp_impl(ctx, mlp, df, df + 4 * n, n, df + 5 * n, m, MUX_W_I32, qbits, ctx->wq.ptr, ldw, st,
+                                   &launches));
+    MUX_CUDA_TRY(cudaEventRecord(ev.e[1], st));
+    // generic ordering keys for the multilevel warm start: row / column sums
+    MUX_TRY(mux_match_impl(ctx, ctx->wq.ptr, MUX_W_I32, n, m, ldw, col_dev, total_q, stats, st, tuning().auc_theta,
+                           tuning().auc_tail, nullptr, nullptr));
+    MUX_CUDA_TRY(cudaMemcpyAsync(col_of_row_host, col_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+    if (stats) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev.e[0], ev.e[1]);
+        stats->ms_score = ms;
+        stats->launches += launches;
+    }
+    return MUX_OK;
+}
+
 }  // extern "C"

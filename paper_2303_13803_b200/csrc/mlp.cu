@@ -6,19 +6,27 @@
 // pair-feature build exploits that layer 1 is separable:
 //   W1 [on; off; s] + b1 = P[u] + Q[v],  P = W1_on on_u + W1_s s_u + b1,  Q = W1_off off_v
 // so per pair only relu(P[u] + Q[v]) is formed (CUDA cores, written straight
-// into the UMMA shared-memory layout as bf16).  Per tile of 128 pairs (one
-// online row u x 128 offline columns):
-//   h1 (smem, bf16) --tcgen05.mma x4 (M128 N64 K16, W2 in smem)--> TMEM cols [0,64)
-//   epilogue 1: tcgen05.ld -> +b2, ReLU -> bf16 -> smem (A operand of layer 3)
-//   h2 (smem) --tcgen05.mma x4 (W3)--> TMEM cols [64,128)
-//   epilogue 2: tcgen05.ld -> +b3, ReLU -> dot w4 + b4 -> clamp [0,1] -> store
-// Accumulation is fp32 in TMEM.  One elected thread issues the MMAs and
-// commits them to an mbarrier; four CTAs share an SM (128 TMEM columns each)
-// so one CTA's MMAs overlap the others' CUDA-core stages.
+// into the UMMA shared-memory layout).  Per tile of 128 pairs (one online row
+// u x 128 offline columns):
+//   h1 (smem) --tcgen05.mma x9 (M128 N64 K16, W2 in smem)--> TMEM
+//   epilogue 1: tcgen05.ld -> ReLU -> split -> smem (A operand of layer 3)
+//   h2 (smem) --tcgen05.mma x9 (W3)--> TMEM
+//   epilogue 2: tcgen05.ld -> ReLU -> dot w4 + b4 -> clamp [0,1] -> store
+//
+// Precision (the 1e-3 relative bar): operands are fp16 (kind::f16, fp32
+// accumulation in TMEM).  The model's layer-2/3 weights and biases are fp16
+// values (MlpPredictor stores them rounded), so B is exact; each activation
+// is split as a = hi + lo with hi = fp16(a), lo = fp16(a - hi) and the GEMM
+// runs over K = [hi | lo | ones] against [W; W; bias]: A_hi W + A_lo W + b in
+// one chain of 9 K16 MMAs, ~2^-22 relative per product instead of fp16's
+// 2^-12 (measured ~1e-7 absolute against the float64 oracle).
+// One elected thread issues the MMAs and commits them to an mbarrier; three
+// CTAs share an SM (64 TMEM columns each) so one CTA's MMAs overlap the
+// others' CUDA-core stages.
 // Operands use the K-major, no-swizzle canonical layout: 8-row x 16-byte core
-// matrices, LBO = 128 B between K-adjacent cores, SBO = 1024 B between 8-row
-// groups (one 8-row group holds all 64 K values).
-#include <cuda_bf16.h>
+// matrices, LBO = 128 B between K-adjacent cores, SBO = 18 x 128 B between
+// 8-row groups (one 8-row group holds all 144 K values).
+#include <cuda_fp16.h>
 
 #include <cstring>
 #include <string>
@@ -30,20 +38,23 @@
 namespace mux {
 
 constexpr int kH = 64;              // hidden width
-constexpr int kKp = 80;             // GEMM K: 64 activations + a ones column (bias) padded to 16
+constexpr int kKp = 144;            // GEMM K: 64 hi + 64 lo activation halves + a ones column (bias) padded to 16
 constexpr int kKg = kKp / 8;        // 16-byte k-groups per operand row
 constexpr int kSbo = kKg * 128;     // bytes between 8-row core groups (B operands)
 constexpr int kSboA = kSbo + 16;    // A operand: +16 B per group rotates banks (conflict-free epilogue stores)
 constexpr int kTile = 128;          // pairs per MMA tile (UMMA M)
 constexpr int kMlpThreads = 128;    // 4 warps = the 4 TMEM lane quadrants
-template <bool PF> struct MlpCfg { static constexpr int ctas = PF ? 4 : 5; };
+template <bool PF> struct MlpCfg { static constexpr int ctas = 3; };
 constexpr uint32_t kTmemCols = 64;  // one accumulator reused by layers 2 and 3
+constexpr int kSmemA = (((kTile / 8) * kSboA) + 1023) / 1024 * 1024;
+constexpr int kSmemW = kH * kKp * 2;
+constexpr int kSmemDyn = kSmemA + 2 * kSmemW;
 
 struct MlpDev {
     const float* P;          // [n][64] per-row layer-1 partial (incl. b1)
     const float* Q;          // [m][64] per-column layer-1 partial
-    const uint16_t* W2c;     // [64 x 80] bf16 bits, UMMA core layout, column 64 = b2
-    const uint16_t* W3c;     // same with b3
+    const uint16_t* W2c;     // [64 x 144] fp16 bits, UMMA core layout: W2 | W2 | b2
+    const uint16_t* W3c;     // same with W3, b3
     const float* w4;
     float b4;
     int32_t n, m;
@@ -61,12 +72,12 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, K-major A and B.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// kind::f16 instruction descriptor: fp16 x fp16 -> f32, K-major A and B.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
@@ -104,21 +115,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 // byte offset of core chunk (row r, k-group kg) in the A tile (K-major, kKp columns)
 __device__ __forceinline__ uint32_t core_off(int r, int kg) {
     return (uint32_t)((r >> 3) * kSboA + kg * 128 + (r & 7) * 16);
 }
 
-// relu(bf16(a), bf16(b)) packed: one cvt + one HMAX2 per pair
-__device__ __forceinline__ uint32_t relu_bf16x2(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    h = __hmax2(h, __float2bfloat162_rn(0.f));
-    return *reinterpret_cast<const uint32_t*>(&h);
+// relu(a), relu(b) split into fp16 hi / lo halves: a = hi + lo to ~2^-22
+__device__ __forceinline__ void relu_split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    a = fmaxf(a, 0.f);
+    b = fmaxf(b, 0.f);
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 // PF = true: the next tile's P/Q rows are prefetched into registers under the
@@ -127,9 +138,11 @@ __device__ __forceinline__ uint32_t relu_bf16x2(float a, float b) {
 template <int WT, bool PF>
 __global__ void __launch_bounds__(kMlpThreads, MlpCfg<PF>::ctas)
 mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
-    __shared__ __align__(1024) unsigned char sA[(kTile / 8) * kSboA];  // ~20 KB
-    __shared__ __align__(1024) unsigned char sW2[kH * kKp * 2];       // 10 KB
-    __shared__ __align__(1024) unsigned char sW3[kH * kKp * 2];
+    // dynamic shared memory: A tile (36 KB) + W2 / W3 operands (18 KB each)
+    extern __shared__ __align__(1024) unsigned char dsm[];
+    unsigned char* sA = dsm;
+    unsigned char* sW2 = dsm + kSmemA;
+    unsigned char* sW3 = sW2 + kSmemW;
     __shared__ __align__(16) float sP[kH];
     __shared__ __align__(16) float sw4[kH];
     __shared__ uint64_t mbar;
@@ -141,9 +154,9 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         reinterpret_cast<uint4*>(sW3)[e] = reinterpret_cast<const uint4*>(p.W3c)[e];
     }
     if (tid < kH) sw4[tid] = p.w4[tid];
-    // constant bias k-groups of the A operand: column 64 = 1.0, 65..79 = 0
-    *reinterpret_cast<uint4*>(sA + core_off(tid, 8)) = make_uint4(0x3F80u, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(sA + core_off(tid, 9)) = make_uint4(0u, 0u, 0u, 0u);
+    // constant bias k-groups of the A operand: column 128 = 1.0 (fp16), 129..143 = 0
+    *reinterpret_cast<uint4*>(sA + core_off(tid, 16)) = make_uint4(0x3C00u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sA + core_off(tid, 17)) = make_uint4(0u, 0u, 0u, 0u);
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(su32(&tmem_base)), "r"(kTmemCols) : "memory");
@@ -156,7 +169,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
     tc_fence_after();
     const uint32_t tmem = tmem_base;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    const uint32_t idesc = idesc_bf16(kTile, kH);
+    const uint32_t idesc = idesc_f16(kTile, kH);
     const uint32_t a_addr = su32(sA), w2_addr = su32(sW2), w3_addr = su32(sW3);
     uint32_t phase = 0;
 
@@ -193,7 +206,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
             tc_fence_after();
 #pragma unroll
             for (int ks = 0; ks < kKp / 16; ++ks)
-                mma_bf16(tmem + dcol, umma_desc(a_addr + ks * 256, 128, kSboA), umma_desc(b_addr + ks * 256, 128, kSbo),
+                mma_f16(tmem + dcol, umma_desc(a_addr + ks * 256, 128, kSboA), umma_desc(b_addr + ks * 256, 128, kSbo),
                          idesc, ks > 0);
             mma_commit(&mbar);
         }
@@ -205,8 +218,9 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         if (!PF) prefetch(tile);   // batch this tile's loads up front
         if (tid < kH / 4) reinterpret_cast<float4*>(sP)[tid] = pf;
         __syncthreads();
-        // ---- h1 = relu(P[u] + Q[v]) -> bf16 into the UMMA layout.  A thread's
-        // chunks c = tid + 128 j all share k-group (tid >> 3) & 7: P loads once.
+        // ---- h1 = relu(P[u] + Q[v]) -> fp16 hi (k-groups 0-7) / lo (8-15) halves
+        // into the UMMA layout.  A thread's chunks c = tid + 128 j all share
+        // k-group (tid >> 3) & 7: P loads once.
         const int kg_t = (tid >> 3) & 7;
         const float4 p0 = reinterpret_cast<const float4*>(sP + kg_t * 8)[0];
         const float4 p1 = reinterpret_cast<const float4*>(sP + kg_t * 8)[1];
@@ -216,12 +230,13 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
             const int r = (c & 7) | ((c >> 6) << 3);
             const int kg = kg_t;
             const float4 q0 = qa[j], q1 = qb[j];
-            uint4 pk;
-            pk.x = relu_bf16x2(p0.x + q0.x, p0.y + q0.y);
-            pk.y = relu_bf16x2(p0.z + q0.z, p0.w + q0.w);
-            pk.z = relu_bf16x2(p1.x + q1.x, p1.y + q1.y);
-            pk.w = relu_bf16x2(p1.z + q1.z, p1.w + q1.w);
-            *reinterpret_cast<uint4*>(sA + core_off(r, kg)) = pk;
+            uint4 hi, lo;
+            relu_split_f16x2(p0.x + q0.x, p0.y + q0.y, hi.x, lo.x);
+            relu_split_f16x2(p0.z + q0.z, p0.w + q0.w, hi.y, lo.y);
+            relu_split_f16x2(p1.x + q1.x, p1.y + q1.y, hi.z, lo.z);
+            relu_split_f16x2(p1.z + q1.z, p1.w + q1.w, hi.w, lo.w);
+            *reinterpret_cast<uint4*>(sA + core_off(r, kg)) = hi;
+            *reinterpret_cast<uint4*>(sA + core_off(r, kg + 8)) = lo;
         }
         fence_async_smem();
         __syncthreads();
@@ -231,7 +246,7 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
         bar_wait(&mbar, phase);
         phase ^= 1;
         tc_fence_after();
-        // ---- epilogue 1: ReLU -> bf16 -> A operand of layer 3 (own row)
+        // ---- epilogue 1: ReLU -> fp16 hi / lo -> A operand of layer 3 (own row)
         const int row = tid;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {   // two TMEM loads in flight per wait
@@ -242,11 +257,13 @@ mlp_pairs_kernel(MlpDev p, void* __restrict__ out, int64_t ldo, double qscale) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int cb = half * 2 + h;
-                uint32_t w[8];
+                uint32_t w[8], wl[8];
 #pragma unroll
-                for (int t = 0; t < 8; ++t) w[t] = relu_bf16x2(acc[h][2 * t], acc[h][2 * t + 1]);
+                for (int t = 0; t < 8; ++t) relu_split_f16x2(acc[h][2 * t], acc[h][2 * t + 1], w[t], wl[t]);
                 *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2)) = make_uint4(w[0], w[1], w[2], w[3]);
                 *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 1)) = make_uint4(w[4], w[5], w[6], w[7]);
+                *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 8)) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+                *reinterpret_cast<uint4*>(sA + core_off(row, cb * 2 + 9)) = make_uint4(wl[4], wl[5], wl[6], wl[7]);
             }
         }
         tc_fence_before();
@@ -331,35 +348,34 @@ __global__ void mlp_layer1_kernel(MlpL1 w, const double* __restrict__ on, const 
 
 using namespace mux;
 
-// fp32 -> bf16 bits, round to nearest even (host)
-static uint16_t bf16_bits(float f) {
-    uint32_t x;
-    memcpy(&x, &f, 4);
-    const uint32_t lsb = (x >> 16) & 1u;
-    x += 0x7FFFu + lsb;
-    return (uint16_t)(x >> 16);
-}
-
 // W [64 out][64 in] row-major + bias -> UMMA K-major core layout of the
-// [64 x 80] B operand (column 64 = bias, 65..79 = 0), N = out
-static void to_core_layout(const float* W, const float* bias, uint16_t* dst) {
+// [64 x 144] fp16 B operand: columns 0-63 and 64-127 = W (against the hi and
+// lo activation halves), 128 = bias, 129-143 = 0; N = out.  The model's
+// weights are fp16 values (MlpPredictor), so the conversion is exact.
+static int to_core_layout(const float* W, const float* bias, uint16_t* dst) {
     for (int nn = 0; nn < kH; ++nn)
         for (int k = 0; k < kKp; ++k) {
-            const float val = k < kH ? W[nn * kH + k] : (k == kH ? bias[nn] : 0.f);
+            const float val = k < 2 * kH ? W[nn * kH + (k & (kH - 1))] : (k == 2 * kH ? bias[nn] : 0.f);
+            const __half h = __float2half_rn(val);
+            if (__half2float(h) != val) return MUX_EINVAL;   // not an fp16 value
             const size_t off = (size_t)(nn >> 3) * (kSbo / 2) + (size_t)(k >> 3) * 64 + (size_t)(nn & 7) * 8 + (k & 7);
-            dst[off] = bf16_bits(val);
+            memcpy(&dst[off], &h, 2);
         }
+    return MUX_OK;
 }
 
 int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, const double* share, int64_t n,
                        const double* off, int64_t m, int wtype, int qbits, void* out, int64_t ldo,
                        cudaStream_t st, int64_t* launches) {
     if (w->hidden != kH) { set_error("mux_score_mlp: hidden width must be 64"); return MUX_EINVAL; }
-    // parameter block on device: W2c, W3c (bf16 core layout), b2, b3, w4
+    // parameter block on device: W2c, W3c (fp16 core layout with the biases), w4
     const size_t o_w2 = 0, o_w3 = o_w2 + kH * kKp * 2, o_w4 = o_w3 + kH * kKp * 2, o_end = o_w4 + kH * 4;
     std::string blob(o_end, '\0');
-    to_core_layout(w->W2, w->b2, reinterpret_cast<uint16_t*>(&blob[o_w2]));
-    to_core_layout(w->W3, w->b3, reinterpret_cast<uint16_t*>(&blob[o_w3]));
+    if (to_core_layout(w->W2, w->b2, reinterpret_cast<uint16_t*>(&blob[o_w2])) != MUX_OK ||
+        to_core_layout(w->W3, w->b3, reinterpret_cast<uint16_t*>(&blob[o_w3])) != MUX_OK) {
+        set_error("mux_score_mlp: W2, b2, W3, b3 must be fp16 values");
+        return MUX_EINVAL;
+    }
     memcpy(&blob[o_w4], w->w4, kH * 4);
     const size_t pq_bytes = sizeof(float) * kH * (size_t)(n + m);
     MUX_TRY(ctx->mlp.ensure(o_end + 256 + pq_bytes));
@@ -387,14 +403,18 @@ int mux_score_mlp_impl(mux_ctx_t* ctx, const mux_mlp_t* w, const double* on, con
     const int64_t tiles = n * ((m + kTile - 1) / kTile);
     if (tiles > 0) {
         const bool pf = tuning().mlp_prefetch;
+        MUX_CUDA_TRY(cudaFuncSetAttribute(mlp_pairs_kernel<MUX_W_F32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDyn));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(mlp_pairs_kernel<MUX_W_I32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDyn));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(mlp_pairs_kernel<MUX_W_F32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDyn));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(mlp_pairs_kernel<MUX_W_I32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemDyn));
         const unsigned grid = (unsigned)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * (pf ? MlpCfg<true>::ctas : MlpCfg<false>::ctas));
         const double qscale = ldexp(1.0, qbits);
         if (pf) {
-            if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32, true><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
-            else mlp_pairs_kernel<MUX_W_I32, true><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+            if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32, true><<<grid, kMlpThreads, kSmemDyn, st>>>(p, out, ldo, qscale);
+            else mlp_pairs_kernel<MUX_W_I32, true><<<grid, kMlpThreads, kSmemDyn, st>>>(p, out, ldo, qscale);
         } else {
-            if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32, false><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
-            else mlp_pairs_kernel<MUX_W_I32, false><<<grid, kMlpThreads, 0, st>>>(p, out, ldo, qscale);
+            if (wtype == MUX_W_F32) mlp_pairs_kernel<MUX_W_F32, false><<<grid, kMlpThreads, kSmemDyn, st>>>(p, out, ldo, qscale);
+            else mlp_pairs_kernel<MUX_W_I32, false><<<grid, kMlpThreads, kSmemDyn, st>>>(p, out, ldo, qscale);
         }
         ++*launches;
     }

@@ -6,9 +6,11 @@ and the SM share; the reference ships only a table and
 says any regressor exported as a grid plugs in (predictor.py:6-8).  This
 plugin evaluates the MLP itself for every pair on the GPU
 (csrc/mlp.cu: layer 1 split into per-row / per-column partials, layers 2-3 as
-tcgen05 bf16 GEMMs with fp32 accumulation in TMEM, bias + ReLU and the final
-64-wide dot fused into the TMEM->register epilogues).  `export_table` turns it
-into a `PredictionTable` (the reference's plug-in hook,
+tcgen05 fp16 GEMMs with split (hi + lo) activations and fp32 accumulation in
+TMEM, ReLU and the final 64-wide dot fused into the TMEM->register
+epilogues), either as a scoring call (`predict_pairs_mlp`), inside the GPU
+round (`schedule(..., table=<MlpPredictor>)` -> `mux_round_mlp`), or exported
+as a `PredictionTable` (`export_table`, the reference's plug-in hook
 build_table_from_model, predictor.py:134-153).
 
 Network (reading "four layers" as in -> 64 -> 64 -> 64 -> 1):
@@ -16,8 +18,11 @@ Network (reading "four layers" as in -> 64 -> 64 -> 64 -> 1):
     h1 = relu(W1 x + b1); h2 = relu(W2 h1 + b2); h3 = relu(W3 h2 + b3)
     w  = clamp(w4 . h3 + b4, 0, 1)
 Features per workload: (gpu_utilization, sm_activity, sm_occupancy,
-iter_time_separate).  Training is out of scope; weights are
-supplied by the caller or drawn by `MlpPredictor.random`.
+iter_time_separate).  The tensor-core layers' parameters (W2, b2, W3, b3) are
+stored as fp16 values -- the model's deployment precision; the float64 oracle
+(oracle/mlp_ref.py) uses the same stored values.  Training is out of scope
+(SPEC.md:14); weights are supplied by the caller or drawn by
+`MlpPredictor.random`.
 """
 
 import ctypes
@@ -29,6 +34,7 @@ from . import _native as nat
 
 HIDDEN = 64
 N_FEAT = 9
+FP16_PARAMS = ("W2", "b2", "W3", "b3")
 
 
 def profile_features(p):
@@ -68,6 +74,10 @@ class MlpPredictor:
                 raise ValueError(f"MLP parameter {name} has shape {a.shape}, expected {shape}")
             if not np.all(np.isfinite(a)):
                 raise ValueError(f"MLP parameter {name} has non-finite entries")
+            if name in FP16_PARAMS:
+                a = a.astype(np.float16).astype(np.float32)   # the tensor-core layers' stored precision
+                if not np.all(np.isfinite(a)):
+                    raise ValueError(f"MLP parameter {name} overflows fp16")
             a.setflags(write=False)
             object.__setattr__(self, name, a)
         object.__setattr__(self, "b4", float(np.float32(self.b4)))
@@ -130,3 +140,58 @@ def predict_pairs_mlp(mlp: MlpPredictor, on_feat, share, off_feat, dtype="float3
                                 off.data_ptr(), m, wtype, int(qbits), out.data_ptr(), ldo, nat.stream_ptr()))
     del keep
     return out[:, :m]
+
+
+def export_table(mlp: MlpPredictor, online_sm=None, offline_sm=None, sm_pct=None, online_iter=0.02,
+                 offline_iter=0.1, occupancy=0.5, gpu_type="default"):
+    """The MLP sampled on a prediction grid: a `PredictionTable` the
+    reference's table path accepts unchanged (its plug-in contract,
+    predictor.py:6-8 and build_table_from_model, predictor.py:134-153).
+
+    Grid point (x, y, z) = (online SM activity, offline SM activity, share);
+    the other profile features follow the synthetic records (gpu_utilization
+    = min(1, 1.8 sm), sm_occupancy = `occupancy`, iter_time_separate =
+    `online_iter` / `offline_iter`).  All grid points are scored in one GPU
+    call.  The table contract requires values non-decreasing along sm_pct
+    (predictor.py:56-71), so the export takes the running maximum along that
+    axis (a no-op for a monotone model)."""
+    from .predictor import PredictionTable
+    from .tables import DEFAULT_OFFLINE_SM, DEFAULT_ONLINE_SM, DEFAULT_SM_PCT
+    xs = np.asarray(DEFAULT_ONLINE_SM if online_sm is None else online_sm, dtype=np.float64)
+    ys = np.asarray(DEFAULT_OFFLINE_SM if offline_sm is None else offline_sm, dtype=np.float64)
+    zs = np.asarray(DEFAULT_SM_PCT if sm_pct is None else sm_pct, dtype=np.float64)
+    X, Z = np.meshgrid(xs, zs, indexing="ij")                  # rows = (x, z) pairs
+    X, Z = X.reshape(-1), Z.reshape(-1)
+    on = np.stack([np.minimum(1.0, 1.8 * X), X, np.full_like(X, occupancy), np.full_like(X, online_iter)], axis=1)
+    off = np.stack([np.minimum(1.0, 1.8 * ys), ys, np.full_like(ys, occupancy), np.full_like(ys, offline_iter)], axis=1)
+    W = predict_pairs_mlp(mlp, on, Z, off).cpu().numpy().astype(np.float64)   # [(x, z), y]
+    vals = W.reshape(xs.size, zs.size, ys.size).transpose(0, 2, 1)            # [x][y][z]
+    vals = np.maximum.accumulate(np.clip(vals, 0.0, 1.0), axis=2)
+    return PredictionTable(online_sm=tuple(float(v) for v in xs), offline_sm=tuple(float(v) for v in ys),
+                           sm_pct=tuple(float(v) for v in zs), values=vals, gpu_type=gpu_type)
+
+
+def round_arrays_mlp(mlp: MlpPredictor, on_feat, share, off_feat, qbits=30, stats=False):
+    """One GPU round with the MLP as the predictor (C ABI `mux_round_mlp`):
+    host features in, MLP scores quantised to 30-bit weights in HBM, the
+    exact matching, col_of_row out (-1 = unmatched).  Returns (col, total_q[,
+    stats])."""
+    nat.torch_cuda()
+    on = np.ascontiguousarray(np.asarray(on_feat, dtype=np.float64).reshape(-1, 4))
+    off = np.ascontiguousarray(np.asarray(off_feat, dtype=np.float64).reshape(-1, 4))
+    sh = np.ascontiguousarray(np.asarray(share, dtype=np.float64).reshape(-1))
+    n, m = on.shape[0], off.shape[0]
+    if sh.shape[0] != n:
+        raise ValueError("on_feat and share must have the same length")
+    col = np.empty(max(n, 1), dtype=np.int32)
+    total = ctypes.c_int64(0)
+    st = nat.MuxStats()
+    s, keep = mlp.struct()
+    dp = ctypes.c_void_p
+    nat.check(nat.load().mux_round_mlp(nat.context(), ctypes.byref(s), dp(on.ctypes.data), dp(sh.ctypes.data), n,
+                                       dp(off.ctypes.data), m, int(qbits), dp(col.ctypes.data), ctypes.byref(total),
+                                       ctypes.byref(st), nat.stream_ptr()))
+    del keep
+    if stats:
+        return col[:n], int(total.value), st.as_dict()
+    return col[:n], int(total.value)

@@ -1,12 +1,12 @@
 """MLP plugin (tcgen05 kernel) against its float64 oracle.  Parity is
 UNPINNED relative to the reference (which has no MLP); the oracle is
-oracle/mlp_ref.py on the same weights.
+oracle/mlp_ref.py on the same weights (W2, b2, W3, b3 are stored as fp16
+values by MlpPredictor, and the oracle uses the stored values).
 
-Two checks: (1) against a numpy emulation of the kernel's precision (bf16
-rounding of the layer-1/2 activations and of W2/W3, fp32 elsewhere) -- this
-pins the tensor-core data path to 1e-4; (2) against the pure float64 network
--- this measures what bf16 operands cost (documented bound: 2e-2 absolute on
-outputs in [0, 1])."""
+The north-star bar is 1e-3 relative; the kernel's split (hi + lo) fp16
+activations with fp32 accumulation give ~1e-7 absolute, so the tests assert
+|gpu - oracle| <= 1e-3 |oracle| + 1e-6 and, as a regression guard, a 2e-6
+absolute maximum."""
 
 import numpy as np
 import pytest
@@ -16,32 +16,10 @@ from oracle import mlp_ref
 pytestmark = pytest.mark.gpu
 
 
-def bf16(x):
-    x = np.asarray(x, dtype=np.float32)
-    b = x.view(np.uint32).astype(np.uint64)
-    r = ((b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
-    return r.view(np.float32)
-
-
-def emulated(params, on, share, off):
-    """Kernel-precision forward: P/Q fp32, h1/W2/h2/W3 and the layer-2/3
-    biases bf16 (they ride in the GEMM as a ones column), fp32 accumulate."""
-    f32 = np.float32
-    W1 = params["W1"].astype(f32)
-    shift, scale = params["shift"].astype(f32), params["scale"].astype(f32)
-    x_on = ((on - shift[:4].astype(np.float64)) * scale[:4].astype(np.float64)).astype(f32)
-    x_off = ((off - shift[4:8].astype(np.float64)) * scale[4:8].astype(np.float64)).astype(f32)
-    x_s = ((share - float(shift[8])) * float(scale[8])).astype(f32)
-    P = x_on @ W1[:, :4].T + x_s[:, None] * W1[:, 8][None, :] + params["b1"].astype(f32)
-    Q = x_off @ W1[:, 4:8].T
-    W2, W3 = bf16(params["W2"]), bf16(params["W3"])
-    out = np.empty((P.shape[0], Q.shape[0]), dtype=np.float64)
-    for u in range(P.shape[0]):
-        h1 = bf16(np.maximum(P[u][None, :] + Q, 0))
-        h2 = bf16(np.maximum(h1 @ W2.T + bf16(params["b2"]), 0))
-        h3 = np.maximum(h2 @ W3.T + bf16(params["b3"]), 0)
-        out[u] = np.clip(h3 @ params["w4"].astype(f32) + f32(params["b4"]), 0, 1)
-    return out
+def _close(W, R):
+    d = np.abs(W - R)
+    assert np.all(d <= 1e-3 * np.abs(R) + 1e-6), f"max rel {np.max(d / np.maximum(np.abs(R), 1e-12)):.3e}"
+    assert d.max() < 2e-6, f"max abs {d.max():.3e}"
 
 
 def _inputs(n, m, seed):
@@ -54,28 +32,37 @@ def _inputs(n, m, seed):
     return on, share, off
 
 
-@pytest.mark.parametrize("n,m,seed", [(1, 1, 0), (3, 129, 1), (130, 300, 2), (257, 1000, 3)])
-def test_mlp_kernel_matches_emulation(cuda, n, m, seed):
+@pytest.mark.parametrize("n,m,seed", [(1, 1, 0), (3, 129, 1), (130, 300, 2), (257, 1000, 3), (200, 700, 7)])
+def test_mlp_kernel_vs_float64(cuda, n, m, seed):
     from paper_2303_13803_b200.mlp import MlpPredictor, predict_pairs_mlp
     mlp = MlpPredictor.random(seed)
     on, share, off = _inputs(n, m, seed)
     W = predict_pairs_mlp(mlp, on, share, off).cpu().numpy().astype(np.float64)
-    E = emulated(mlp.params(), on, share, off)
-    d = np.abs(W - E)
-    # fp32 accumulation order can flip one bf16 rounding of an activation:
-    # nearly every entry agrees to fp32 precision, a few move by ~1 bf16 ulp
-    assert np.quantile(d, 0.99) < 1e-5
-    assert d.max() < 5e-3
+    R = mlp_ref.forward(mlp.params(), on, share, off)
+    _close(W, R)
 
 
-def test_mlp_kernel_vs_float64(cuda):
-    from paper_2303_13803_b200.mlp import MlpPredictor, predict_pairs_mlp
+def test_mlp_outputs_span_the_unit_interval(cuda):
+    from paper_2303_13803_b200.mlp import MlpPredictor
     mlp = MlpPredictor.random(7)
     on, share, off = _inputs(200, 700, 7)
-    W = predict_pairs_mlp(mlp, on, share, off).cpu().numpy().astype(np.float64)
     R = mlp_ref.forward(mlp.params(), on, share, off)
     assert 0.05 < R.mean() < 0.95          # the random net spans (0, 1)
-    assert np.max(np.abs(W - R)) < 2e-2
+
+
+def test_mlp_rejects_non_fp16_tensor_layer_weights(cuda):
+    import ctypes
+    from paper_2303_13803_b200 import _native as nat
+    from paper_2303_13803_b200.mlp import MlpPredictor
+    mlp = MlpPredictor.random(1)
+    s, keep = mlp.struct()
+    keep["W2"][0, 0] = np.float32(1.0 + 2.0 ** -20)        # not an fp16 value
+    out = __import__("torch").empty((1, 4), dtype=__import__("torch").float32, device="cuda")
+    on = __import__("torch").zeros((1, 4), dtype=__import__("torch").float64, device="cuda")
+    sh = __import__("torch").zeros(1, dtype=__import__("torch").float64, device="cuda")
+    rc = nat.load().mux_score_mlp(nat.context(), ctypes.byref(s), on.data_ptr(), sh.data_ptr(), 1, on.data_ptr(), 1,
+                                  nat.MUX_W_F32, 0, out.data_ptr(), 4, nat.stream_ptr())
+    assert rc == nat.MUX_EINVAL
 
 
 def test_mlp_quantised_output_and_matching(cuda):
@@ -95,3 +82,41 @@ def test_mlp_quantised_output_and_matching(cuda):
     col, total = match_dense(full)
     opt, _ = matching_ref.max_weight_total_int(Qh)
     assert total == opt
+
+
+def test_mlp_round_through_the_c_abi(cuda):
+    """mux_round_mlp: host features -> MLP scores (30-bit weights) -> exact matching."""
+    from paper_2303_13803_b200.mlp import MlpPredictor, predict_pairs_mlp, round_arrays_mlp
+    from oracle import matching_ref
+    mlp = MlpPredictor.random(4)
+    on, share, off = _inputs(300, 450, 4)
+    col, total = round_arrays_mlp(mlp, on, share, off, qbits=30)
+    Q = predict_pairs_mlp(mlp, on, share, off, dtype="int32", qbits=30).cpu().numpy().astype(np.int64)
+    from scipy.optimize import linear_sum_assignment
+    r, c = linear_sum_assignment(Q.astype(np.float64), maximize=True)
+    assert total == int(Q[r, c].sum())
+    assert matching_ref.assignment_total_int(Q, col) == total
+
+
+def test_schedule_with_the_mlp_plugin_and_its_exported_table(cuda):
+    """schedule() takes the MLP in place of the table (the reference's plug-in
+    contract, predictor.py:6-8); export_table turns it into a PredictionTable
+    the table path accepts, bit-identical to the MLP at the grid points."""
+    from paper_2303_13803_b200 import SchedulerConfig, predict_point, schedule
+    from paper_2303_13803_b200.mlp import MlpPredictor, export_table, predict_pairs_mlp
+    from paper_2303_13803_b200.synth import make_cluster, records
+    mlp = MlpPredictor.random(5)
+    cl = make_cluster(120, 90, seed=5)
+    onl, off, states = records(cl)
+    asg = schedule(onl, off, states, mlp, SchedulerConfig(), 900.0)
+    assert len(asg.pairs) == 90 and len(asg.unplaced) == 0
+    t = export_table(mlp)
+    xs, ys, zs = np.array(t.online_sm), np.array(t.offline_sm), np.array(t.sm_pct)
+    on = np.stack([np.minimum(1.0, 1.8 * xs), xs, np.full_like(xs, 0.5), np.full_like(xs, 0.02)], axis=1)
+    offf = np.stack([np.minimum(1.0, 1.8 * ys), ys, np.full_like(ys, 0.5), np.full_like(ys, 0.1)], axis=1)
+    k = 3
+    W = predict_pairs_mlp(mlp, on, np.full(xs.size, zs[k]), offf).cpu().numpy()
+    assert np.all(t.values[:, :, k] >= np.clip(W, 0, 1) - 1e-12)
+    assert abs(predict_point(t, xs[2], ys[4], zs[k]) - t.values[2, 4, k]) == 0.0
+    asg2 = schedule(onl, off, states, t, SchedulerConfig(), 900.0)
+    assert len(asg2.pairs) == 90
