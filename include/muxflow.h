@@ -239,6 +239,18 @@ int mux_round_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp,
                   int32_t* col_of_row_host, int64_t* total_q,
                   mux_stats_t* stats, void* stream);
 
+/*
+ * Multi-GPU row-sharded scoring without a gather (one process per GPU,
+ * sharded.py): the root exports a device buffer for the weight matrix
+ * (allocated by the context, `bytes` long; handle_out receives the 64-byte
+ * cudaIpcMemHandle), every other rank imports it (peer-mapped over NVLink,
+ * one mapping per context) and passes `dev_ptr + its row offset` as the
+ * out_dev of mux_score_table, so the scoring kernel's stores land in the
+ * root's HBM directly.
+ */
+int mux_ipc_export(mux_ctx_t* ctx, int64_t bytes, void** dev_ptr, void* handle_out);
+int mux_ipc_import(mux_ctx_t* ctx, const void* handle, void** dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

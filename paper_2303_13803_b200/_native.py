@@ -20,7 +20,7 @@ MUX_SCORE_EXACT, MUX_SCORE_FAST = 0, 1
 # every symbol include/muxflow.h declares (checked by tests/test_native_abi.py)
 EXPORTS = ("mux_version", "mux_last_error", "mux_ctx_create", "mux_ctx_destroy",
            "mux_table_validate", "mux_score_table", "mux_score_mlp", "mux_match", "mux_match_keyed",
-           "mux_round", "mux_round_dev", "mux_round_mlp")
+           "mux_round", "mux_round_dev", "mux_round_mlp", "mux_ipc_export", "mux_ipc_import")
 
 
 class MuxTable(ctypes.Structure):
@@ -94,6 +94,8 @@ def load():
                                       P, P, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(MuxStats), P]
         lib.mux_round_mlp.argtypes = [P, P, P, P, i64, P, i64, ctypes.c_int, P, ctypes.POINTER(i64),
                                       ctypes.POINTER(MuxStats), P]
+        lib.mux_ipc_export.argtypes = [P, i64, ctypes.POINTER(P), P]
+        lib.mux_ipc_import.argtypes = [P, P, ctypes.POINTER(P)]
         for name in EXPORTS[2:]:
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib

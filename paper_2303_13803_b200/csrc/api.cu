@@ -179,7 +179,8 @@ int mux_ctx_create(int device, mux_ctx_t** out) {
 int mux_ctx_destroy(mux_ctx_t* ctx) {
     if (!ctx) return MUX_OK;
     cudaSetDevice(ctx->device);
-    for (DevBuf* b : {&ctx->table, &ctx->rowfeat, &ctx->colfeat, &ctx->flags, &ctx->feat_in, &ctx->wq,
+    if (ctx->ipc_in) cudaIpcCloseMemHandle(ctx->ipc_in);
+    for (DevBuf* b : {&ctx->table, &ctx->rowfeat, &ctx->colfeat, &ctx->flags, &ctx->ipc_out, &ctx->feat_in, &ctx->wq,
                       &ctx->colout, &ctx->auc, &ctx->ssp, &ctx->canon, &ctx->canon_ent, &ctx->mlp})
         b->release();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -414,6 +415,28 @@ int mux_round_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp, const double* on_host, c
         stats->ms_score = ms;
         stats->launches += launches;
     }
+    return MUX_OK;
+}
+
+int mux_ipc_export(mux_ctx_t* ctx, int64_t bytes, void** dev_ptr, void* handle_out) {
+    if (!ctx || !dev_ptr || !handle_out || bytes <= 0) { set_error("mux_ipc_export: bad argument"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    MUX_TRY(ctx->ipc_out.ensure((size_t)bytes));
+    cudaIpcMemHandle_t h;
+    MUX_CUDA_TRY(cudaIpcGetMemHandle(&h, ctx->ipc_out.ptr));
+    memcpy(handle_out, &h, sizeof(h));
+    *dev_ptr = ctx->ipc_out.ptr;
+    return MUX_OK;
+}
+
+int mux_ipc_import(mux_ctx_t* ctx, const void* handle, void** dev_ptr) {
+    if (!ctx || !handle || !dev_ptr) { set_error("mux_ipc_import: bad argument"); return MUX_EINVAL; }
+    MUX_CUDA_TRY(cudaSetDevice(ctx->device));
+    if (ctx->ipc_in) { cudaIpcCloseMemHandle(ctx->ipc_in); ctx->ipc_in = nullptr; }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    MUX_CUDA_TRY(cudaIpcOpenMemHandle(&ctx->ipc_in, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = ctx->ipc_in;
     return MUX_OK;
 }
 

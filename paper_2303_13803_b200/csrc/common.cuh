@@ -127,6 +127,8 @@ struct mux_ctx {
     // tie canonicalisation workspace (duals, tight-edge CSR)
     mux::DevBuf canon;
     mux::DevBuf canon_ent;  // tight-edge CSR entries when they outgrow the default buffer
+    mux::DevBuf ipc_out;    // buffer exported to peer processes (mux_ipc_export)
+    void* ipc_in = nullptr; // peer buffer mapped by mux_ipc_import
     // MLP plugin parameters + layer-1 partials
     mux::DevBuf mlp;
     size_t auc_n = 0;

@@ -90,6 +90,27 @@ def match_dense(Wq, n=None, m=None, stats=False):
     return col[:N], int(total.value)
 
 
+def match_dense_ptr(w_ptr, n, m, ldw, rowkey=None, colkey=None):
+    """match_dense on a raw device int32 buffer [n][ldw] (e.g. the root's
+    peer-written weight matrix, sharded.PeerMatrix), optionally ordered by
+    host keys (the online / offline SM demands).  Returns (col int32 CUDA
+    tensor [n], total_q)."""
+    torch = nat.torch_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    col = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    total = nat.ctypes.c_int64(0)
+    st = nat.MuxStats()
+    rk = ck = None
+    if rowkey is not None and colkey is not None:
+        rk = torch.as_tensor(np.ascontiguousarray(rowkey, dtype=np.float64), device=dev)
+        ck = torch.as_tensor(np.ascontiguousarray(colkey, dtype=np.float64), device=dev)
+    nat.check(nat.load().mux_match_keyed(nat.context(), w_ptr, nat.MUX_W_I32, n, m, ldw,
+                                         rk.data_ptr() if rk is not None else None,
+                                         ck.data_ptr() if ck is not None else None, col.data_ptr(), 0,
+                                         nat.ctypes.byref(total), nat.ctypes.byref(st), nat.stream_ptr()))
+    return col[:n], int(total.value)
+
+
 def quantise(W, qbits):
     """Reference edge rule (w < 1e-6 -> missing) then rint(w * 2^qbits)."""
     W = np.asarray(W, dtype=np.float64)

@@ -56,7 +56,10 @@ def test_mlp_rejects_non_fp16_tensor_layer_weights(cuda):
     from paper_2303_13803_b200.mlp import MlpPredictor
     mlp = MlpPredictor.random(1)
     s, keep = mlp.struct()
-    keep["W2"][0, 0] = np.float32(1.0 + 2.0 ** -20)        # not an fp16 value
+    w2 = np.array(keep["W2"], dtype=np.float32)
+    w2[0, 0] = np.float32(1.0 + 2.0 ** -20)                  # not an fp16 value
+    keep["W2"] = w2
+    s.W2 = w2.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
     out = __import__("torch").empty((1, 4), dtype=__import__("torch").float32, device="cuda")
     on = __import__("torch").zeros((1, 4), dtype=__import__("torch").float64, device="cuda")
     sh = __import__("torch").zeros(1, dtype=__import__("torch").float64, device="cuda")
