@@ -423,7 +423,7 @@ def run_ours(args, rank, world, local_rank):
                 ts.append((time.perf_counter() - t0) * 1e3)
             sched_line[f"{k}x{k}"] = {"ms": statistics.median(ts), "pairs": len(asg.pairs),
                                       "qbits": round_qbits(k),
-                                      "solver": "int64 epsilon-scaling auction" if round_qbits(k) > 30 else "multilevel SSP"}
+                                      "solver": "multilevel SSP, int64 weights" if round_qbits(k) > 30 else "multilevel SSP, int32 weights"}
 
     mlp_line = None
     if not args.no_mlp:

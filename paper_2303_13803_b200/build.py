@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmuxflow.so")
-SOURCES = ("api.cu", "score.cu", "auction.cu", "ssp.cu", "canon.cu", "mlp.cu")
+SOURCES = ("api.cu", "score.cu", "auction.cu", "ssp.cu", "ssp_w64.cu", "canon.cu", "mlp.cu")
 HEADERS = ("common.cuh",)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
@@ -30,6 +30,8 @@ def _compile(nvcc, src, obj, force):
     """One translation unit -> object (skipped when the object is newer than
     the source and the shared headers)."""
     deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(HERE, "..", "include", "muxflow.h")]
+    if os.path.basename(src) == "ssp_w64.cu":   # compiles ssp.cu a second time (int64 weights)
+        deps.append(os.path.join(CSRC, "ssp.cu"))
     if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
         return None
     flags = [f for f in NVCC_FLAGS if f != "-shared"]

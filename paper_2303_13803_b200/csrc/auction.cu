@@ -1336,9 +1336,9 @@ __global__ void finalize_kernel(const void* W, int64_t ldw, int32_t N, int32_t M
 }
 
 // out[c][r] = in[r][c] (in: rows x cols, 32 x 32 tiles through shared memory)
-__global__ void transpose_i32_kernel(const int32_t* in, int64_t ldi, int32_t rows, int32_t cols, int32_t* out,
-                                     int64_t ldo) {
-    __shared__ int32_t tile[32][33];
+template <typename T>
+__global__ void transpose_kernel(const T* in, int64_t ldi, int32_t rows, int32_t cols, T* out, int64_t ldo) {
+    __shared__ T tile[32][33];
     const int32_t r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
         const int32_t r = r0 + k, c = c0 + threadIdx.x;
@@ -1352,7 +1352,8 @@ __global__ void transpose_i32_kernel(const int32_t* in, int64_t ldi, int32_t row
 }
 
 // transposed solve (jobs as rows, n = N) -> original orientation
-__global__ void untranspose_duals_kernel(const int32_t* WT, int64_t ldt, int32_t mreal, int32_t n, const int64_t* pT,
+template <typename T>
+__global__ void untranspose_duals_kernel(const T* WT, int64_t ldt, int32_t mreal, int32_t n, const int64_t* pT,
                                          const int32_t* corT, const int32_t* rocT, int64_t sc, int32_t* col,
                                          int64_t* price, int32_t* owner) {
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1364,8 +1365,8 @@ __global__ void untranspose_duals_kernel(const int32_t* WT, int64_t ldt, int32_t
     price[k] = (u >= 0 ? a - pT[u] : 0) * sc;
 }
 
-__global__ void finalize_ssp_kernel(const int32_t* W, int64_t ldw, int32_t N, int32_t M, const int32_t* col,
-                                    int32_t* out) {
+template <typename T>
+__global__ void finalize_ssp_kernel(const T* W, int64_t ldw, int32_t N, int32_t M, const int32_t* col, int32_t* out) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < N) {
         const int32_t j = col[i];
@@ -1392,6 +1393,22 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
                  int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st,
                  const int64_t* price_in = nullptr, const int32_t* warm_col = nullptr);
+int mux_ssp_impl64(mux_ctx_t* ctx, const int64_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
+                   const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
+                   int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st,
+                   const int64_t* price_in = nullptr, const int32_t* warm_col = nullptr);
+
+// the multilevel solver for int32 (csrc/ssp.cu) or int64 (csrc/ssp_w64.cu) weights
+static int ssp_solve(int wtype, mux_ctx_t* ctx, const void* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
+                     const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out, int32_t* cor_out,
+                     int32_t* roc_out, mux_stats_t* stats, cudaStream_t st, const int64_t* price_in = nullptr,
+                     const int32_t* warm_col = nullptr) {
+    if (wtype == MUX_W_I32)
+        return mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, N, M, rowkey, colkey, col_out, total_q, price_out,
+                            cor_out, roc_out, stats, st, price_in, warm_col);
+    return mux_ssp_impl64(ctx, static_cast<const int64_t*>(W), ldw, N, M, rowkey, colkey, col_out, total_q, price_out,
+                          cor_out, roc_out, stats, st, price_in, warm_col);
+}
 
 __global__ void fill_price_kernel(int64_t* p, int32_t n, int64_t v) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1428,7 +1445,9 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
         // N < M: the zero padding rows of the reference's square problem are
         // implicit; N > M: the transposed problem (jobs as rows)
         const bool rect_ok = T.ssp_rect;
-        const bool use_ssp_t = !T.force_auction && wtype == MUX_W_I32 && M >= 1 && N >= 2 && N > M && rect_ok;
+        // int64 weights (qbits 31-44): the solver's 17-bit index keys bound n
+        const bool ssp_w = wtype == MUX_W_I32 || (wtype == MUX_W_I64 && n < 60000);
+        const bool use_ssp_t = !T.force_auction && ssp_w && M >= 1 && N >= 2 && N > M && rect_ok;
         if (use_ssp_t) {
             // N > M: solve the transposed M x N problem (jobs as rows, the padding
             // columns of the reference become implicit zero rows), then map the
@@ -1437,39 +1456,51 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             const int64_t ldt = ((int64_t)nn + 3) / 4 * 4;
             size_t off = 0;
             auto take = [&](size_t b) { size_t o = off; off += (b + 255) & ~(size_t)255; return o; };
-            const size_t o_wt = take(4ull * mm * ldt), o_pt = take(8ull * nn), o_ct = take(4ull * nn),
+            const size_t o_wt = take((size_t)esz * mm * ldt), o_pt = take(8ull * nn), o_ct = take(4ull * nn),
                          o_rt = take(4ull * nn), o_co = take(4ull * nn), o_pr = take(8ull * nn), o_ow = take(4ull * nn);
             MUX_TRY(ctx->auc.ensure(off));
             char* base = ctx->auc.as<char>();
-            int32_t* WT = reinterpret_cast<int32_t*>(base + o_wt);
+            void* WT = base + o_wt;
             int64_t* pT = reinterpret_cast<int64_t*>(base + o_pt);
             int32_t* corT = reinterpret_cast<int32_t*>(base + o_ct);
             int32_t* rocT = reinterpret_cast<int32_t*>(base + o_rt);
             int32_t* colr = reinterpret_cast<int32_t*>(base + o_co);
             int64_t* price = reinterpret_cast<int64_t*>(base + o_pr);
             int32_t* owner = reinterpret_cast<int32_t*>(base + o_ow);
-            transpose_i32_kernel<<<dim3((unsigned)((nn + 31) / 32), (unsigned)((mm + 31) / 32)), dim3(32, 8), 0, st>>>(
-                static_cast<const int32_t*>(W), ldw, nn, mm, WT, ldt);
+            const dim3 tg((unsigned)((nn + 31) / 32), (unsigned)((mm + 31) / 32));
+            if (wtype == MUX_W_I32)
+                transpose_kernel<int32_t><<<tg, dim3(32, 8), 0, st>>>(static_cast<const int32_t*>(W), ldw, nn, mm,
+                                                                     static_cast<int32_t*>(WT), ldt);
+            else
+                transpose_kernel<int64_t><<<tg, dim3(32, 8), 0, st>>>(static_cast<const int64_t*>(W), ldw, nn, mm,
+                                                                     static_cast<int64_t*>(WT), ldt);
             int64_t tq = 0;
-            MUX_TRY(mux_ssp_impl(ctx, WT, ldt, mm, nn, colkey, rowkey, col_out_dev, &tq, pT, corT, rocT, stats, st));
+            MUX_TRY(ssp_solve(wtype, ctx, WT, ldt, mm, nn, colkey, rowkey, col_out_dev, &tq, pT, corT, rocT, stats, st));
             // no column prices to carry in this orientation (the jobs are the rows)
             if (price_io) fill_price_kernel<<<(unsigned)((M + 255) / 256), 256, 0, st>>>(price_io, (int32_t)M, INT64_MIN);
             // original orientation: col_of_row[u] = rocT[u]; owner of job v = corT[v];
             // column (job) prices = the transposed rows' profits
-            untranspose_duals_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(WT, ldt, mm, nn, pT, corT, rocT,
-                                                                                 (int64_t)nn + 1, colr, price, owner);
+            if (wtype == MUX_W_I32)
+                untranspose_duals_kernel<int32_t><<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
+                    static_cast<const int32_t*>(WT), ldt, mm, nn, pT, corT, rocT, (int64_t)nn + 1, colr, price, owner);
+            else
+                untranspose_duals_kernel<int64_t><<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
+                    static_cast<const int64_t*>(WT), ldt, mm, nn, pT, corT, rocT, (int64_t)nn + 1, colr, price, owner);
             if (T.canon)
                 MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, mm, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats));
-            finalize_ssp_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
-                static_cast<const int32_t*>(W), ldw, nn, mm, colr, col_out_dev);
+            if (wtype == MUX_W_I32)
+                finalize_ssp_kernel<int32_t><<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
+                    static_cast<const int32_t*>(W), ldw, nn, mm, colr, col_out_dev);
+            else
+                finalize_ssp_kernel<int64_t><<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
+                    static_cast<const int64_t*>(W), ldw, nn, mm, colr, col_out_dev);
             MUX_CUDA_TRY(cudaGetLastError());
             MUX_CUDA_TRY(cudaStreamSynchronize(st));
             if (stats) { stats->launches += 4; stats->n_rows = N; stats->n_cols = M; stats->total_q = tq; }
             if (total_q) *total_q = tq;
             return MUX_OK;
         }
-        const bool use_ssp = !T.force_auction && wtype == MUX_W_I32 && N >= 1 && M >= 2 &&
-                             (N == M || (N < M && rect_ok));
+        const bool use_ssp = !T.force_auction && ssp_w && N >= 1 && M >= 2 && (N == M || (N < M && rect_ok));
         if (use_ssp) {
             const int32_t nn = (int32_t)M;
             const size_t o_p = 0, o_c = (8ull * nn + 255) & ~255ull, o_o = o_c + ((4ull * nn + 255) & ~255ull);
@@ -1479,9 +1510,8 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             int32_t* colr = reinterpret_cast<int32_t*>(base + o_c);
             int32_t* owner = reinterpret_cast<int32_t*>(base + o_o);
             int64_t tq = 0;
-            MUX_TRY(mux_ssp_impl(ctx, static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, rowkey, colkey, col_out_dev,
-                                 &tq, price, colr, owner, stats, st, (price_io && warm) ? price_io : nullptr,
-                                 (price_io && warm) ? warm_col : nullptr));
+            MUX_TRY(ssp_solve(wtype, ctx, W, ldw, (int32_t)N, nn, rowkey, colkey, col_out_dev, &tq, price, colr, owner,
+                              stats, st, (price_io && warm) ? price_io : nullptr, (price_io && warm) ? warm_col : nullptr));
             // optimal column prices, in quantised-weight units, for the next round's warm start
             if (price_io) MUX_CUDA_TRY(cudaMemcpyAsync(price_io, price, 8ull * (size_t)M, cudaMemcpyDeviceToDevice, st));
             if (T.canon) {
@@ -1490,8 +1520,12 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
                 MUX_TRY(mux_canon_impl(ctx, W, wtype, (int32_t)N, nn, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st,
                                        stats));
                 // the canonical assignment has the same (optimal) total
-                finalize_ssp_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
-                    static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, colr, col_out_dev);
+                if (wtype == MUX_W_I32)
+                    finalize_ssp_kernel<int32_t><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
+                        static_cast<const int32_t*>(W), ldw, (int32_t)N, nn, colr, col_out_dev);
+                else
+                    finalize_ssp_kernel<int64_t><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
+                        static_cast<const int64_t*>(W), ldw, (int32_t)N, nn, colr, col_out_dev);
                 MUX_CUDA_TRY(cudaGetLastError());
                 MUX_CUDA_TRY(cudaStreamSynchronize(st));
                 if (stats) stats->launches += 4;

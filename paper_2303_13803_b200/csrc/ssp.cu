@@ -54,7 +54,25 @@
 namespace cg = cooperative_groups;
 
 namespace mux {
+// One source, two solvers: int32 weights (qbits <= 30; ssp.cu) and int64
+// weights (qbits <= 44, n < 65,000; ssp_w64.cu includes this file with
+// MUX_SSP_W64).  Sort keys pack a value above an index field of kSH bits
+// (the top one a "column is matched" flag): 24 bits for int32 problems, 17
+// for int64 ones, whose values need the extra range.
+#ifndef MUX_SSP_W64
 namespace ssp {
+using wt_t = int32_t;
+constexpr int kSH = 24;
+constexpr int64_t kDistLim = 1ll << 39;
+#else
+namespace ssp64 {
+using wt_t = int64_t;
+constexpr int kSH = 17;
+constexpr int64_t kDistLim = 1ll << 46;
+#endif
+constexpr uint32_t kFreeBit = 1u << (kSH - 1);          // set = matched column (free columns sort first)
+constexpr uint32_t kIdxMask = kFreeBit - 1u;             // column / entry index
+constexpr uint64_t kLowMask = (1ull << kSH) - 1ull;      // flag + index
 
 constexpr int KC = 32;                 // candidates per row record (one per lane)
 constexpr int TC = 256;                // touched columns per warp table (parallel mode)
@@ -63,7 +81,6 @@ constexpr int PWARPS = 8;              // warps per CTA in parallel mode
 constexpr int STEP_BUDGET_DEFAULT = 48;   // Dijkstra pops before a search is deferred
 constexpr int DEEP_BUDGET_DEFAULT = 4;    // dense row re-scans before a search is deferred
 constexpr int MAX_TRIES = 16;          // lock-conflict retries before deferral
-constexpr int64_t kDistLim = 1ll << 39;
 constexpr int64_t kInf = INT64_MAX / 4;
 constexpr uint64_t kNoKey = ~0ull;
 
@@ -85,17 +102,17 @@ struct Cnt {
 };
 
 struct Lvl {
-    const int32_t* A;   // [nreal][lda] benefits; rows >= nreal are zero (the reference's square padding)
+    const wt_t* A;   // [nreal][lda] benefits; rows >= nreal are zero (the reference's square padding)
     int64_t lda;
     int32_t m;
     int32_t nreal;
-    const int32_t* zrow;   // m zeros
+    const wt_t* zrow;   // m zeros
     int64_t* p;         // [m] column prices
     int32_t* cor;       // [m] column of row (-1 free)
     int32_t* roc;       // [m] row of column (-1 free)
     int32_t* lock;      // [m] 0 or owner warp id + 1
     int32_t* cj;        // [m][KC] candidate columns (-1 empty)
-    int32_t* ca;        // [m][KC] their benefits
+    wt_t* ca;           // [m][KC] their benefits
     int64_t* tau;       // [m] bound on every non-candidate value
     const int32_t* in;  // rows to process this pass
     int32_t nin;
@@ -113,7 +130,7 @@ struct Lvl {
     int32_t* xgap;      // global fallback: horizon gaps
 };
 
-__device__ __forceinline__ const int32_t* rowp(const Lvl& L, int32_t i) {
+__device__ __forceinline__ const wt_t* rowp(const Lvl& L, int32_t i) {
     return i < L.nreal ? L.A + (int64_t)i * L.lda : L.zrow;
 }
 
@@ -147,13 +164,13 @@ __device__ __forceinline__ int64_t wmin64s(int64_t v) {
     return v;
 }
 
-// key = (value + 2^39) << 24 | j : ascending key = ascending value, lowest j on ties
+// key = (value + 2^39) << kSH | j : ascending key = ascending value, lowest j on ties
 __device__ __forceinline__ uint64_t mkkey(int64_t v, int32_t j, uint32_t* err) {
     if (v <= -kDistLim || v >= kDistLim) { atomicOr(err, kErrDist); v = v < 0 ? -kDistLim + 1 : kDistLim - 1; }
-    return ((uint64_t)(v + kDistLim) << 24) | (uint64_t)(uint32_t)j;
+    return ((uint64_t)(v + kDistLim) << kSH) | (uint64_t)(uint32_t)j;
 }
-__device__ __forceinline__ int64_t key_val(uint64_t k) { return (int64_t)(k >> 24) - kDistLim; }
-__device__ __forceinline__ int32_t key_idx(uint64_t k) { return (int32_t)(k & 0xFFFFFFu); }
+__device__ __forceinline__ int64_t key_val(uint64_t k) { return (int64_t)(k >> kSH) - kDistLim; }
+__device__ __forceinline__ int32_t key_idx(uint64_t k) { return (int32_t)(k & kLowMask); }
 
 // Warp-wide selection of the 32 smallest keys produced by keyf(j), j in [0, m)
 // (kNoKey = skip).  Lane r receives the r-th smallest (kNoKey when fewer);
@@ -207,7 +224,7 @@ __device__ __forceinline__ void warp_top32(int32_t m, F keyf, uint64_t& mine, ui
 // Rebuild row i's candidate record: its KC best columns by value a_ij - p_j
 // and tau_i >= the value of every other column (prices only rise afterwards).
 __device__ void refresh_row(const Lvl& L, int32_t i) {
-    const int32_t* Ar = rowp(L, i);
+    const wt_t* Ar = rowp(L, i);
     uint64_t mine, bound;
     // plain L2 loads (pipelined): a price read late is still a price the column
     // had, and prices only rise, so tau stays an upper bound
@@ -312,7 +329,7 @@ __device__ __forceinline__ void release_locks(WTab& T, int32_t nt, const Lvl& L)
 // Dense re-scan of row r at base distance db (= d_r + pi_r): its 32 nearest
 // columns not yet scanned join the search; returns the row's new horizon.
 __device__ int64_t deep_relax(WTab& T, int32_t& nt, const Lvl& L, int32_t r, int64_t db, bool& ok) {
-    const int32_t* Ar = rowp(L, r);
+    const wt_t* Ar = rowp(L, r);
     uint64_t mine, bound;
     warp_top32(L.m, [&](int32_t j) -> uint64_t {
         const int32_t e = hfind(T, j);
@@ -366,11 +383,11 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
             const uint8_t f = T.st[e];
             if (f & kScanned) continue;
             const int64_t d = T.dist[e];
-            const uint64_t k = ((uint64_t)(d < kDistLim ? d : kDistLim - 1) << 24) | ((f & kFreeHint) ? 0u : (1u << 23)) | (uint32_t)e;
+            const uint64_t k = ((uint64_t)(d < kDistLim ? d : kDistLim - 1) << kSH) | ((f & kFreeHint) ? 0u : kFreeBit) | (uint32_t)e;
             best = k < best ? k : best;
         }
         best = wmin64(best);
-        const int64_t dmin = best == kNoKey ? kInf : (int64_t)(best >> 24);
+        const int64_t dmin = best == kNoKey ? kInf : (int64_t)(best >> kSH);
         if (dmin > H) {
             // horizon: re-scan every tree row whose bound is below dmin
             bool ok = true;
@@ -407,7 +424,7 @@ __device__ int search(WTab& T, const Lvl& L, int32_t s, int32_t me, unsigned lon
             }
             continue;
         }
-        const int32_t e = (int32_t)(best & 0x7FFFFFu);
+        const int32_t e = (int32_t)(best & kIdxMask);
         const int32_t cc = T.col[e];
         // lock the column (validated price, current owner)
         int32_t ok = 1;
@@ -564,7 +581,7 @@ __device__ __forceinline__ bool x_relax(XTab& X, const Lvl& L, int32_t c, int64_
 // nearer than `thr` joins the search; the row's new horizon is thr.  Callers
 // double the row's reach on each re-scan, so a row is re-scanned O(log) times.
 __device__ int64_t x_deep(XTab& X, const Lvl& L, int32_t r, int64_t db, int64_t thr, bool& ok) {
-    const int32_t* Ar = rowp(L, r);
+    const wt_t* Ar = rowp(L, r);
     constexpr int U = 8;
     for (int32_t j0 = 0; j0 < L.m && ok; j0 += 32 * U) {
         int64_t nd[U];
@@ -627,12 +644,12 @@ __global__ void __launch_bounds__(32, 1) ssp_exclusive_kernel(Lvl L, int32_t nde
             for (int k = lane; k < X.nopen; k += 32) {
                 const int32_t cc = X.ocol[k];
                 const int64_t d = X.dist[cc];
-                const uint64_t key = ((uint64_t)(d < kDistLim ? d : kDistLim - 1) << 24) |
-                                     ((X.flag[cc] & kXFree) ? 0u : (1u << 23)) | (uint32_t)k;
+                const uint64_t key = ((uint64_t)(d < kDistLim ? d : kDistLim - 1) << kSH) |
+                                     ((X.flag[cc] & kXFree) ? 0u : kFreeBit) | (uint32_t)k;
                 best = key < best ? key : best;
             }
             best = wmin64(best);
-            const int64_t dmin = best == kNoKey ? kInf : (int64_t)(best >> 24);
+            const int64_t dmin = best == kNoKey ? kInf : (int64_t)(best >> kSH);
             { const long long c1 = clock64(); cyc[0] += c1 - c0; c0 = c1; }
             if (dmin > H) {
                 // horizon: re-scan the source and every tree row whose bound is below dmin
@@ -670,7 +687,7 @@ __global__ void __launch_bounds__(32, 1) ssp_exclusive_kernel(Lvl L, int32_t nde
                 cyc[1] += clock64() - c0;
                 continue;
             }
-            const int32_t k = (int32_t)(best & 0x7FFFFFu);
+            const int32_t k = (int32_t)(best & kIdxMask);
             const int32_t cc = X.ocol[k];
             __syncwarp();
             if (lane == 0) {
@@ -766,7 +783,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
     unsigned long long steps = 0;
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = rowp(L, s);
+        const wt_t* As = rowp(L, s);
         uint64_t vmin = kNoKey;   // max value as the min of (2^39 - value)
 #pragma unroll
         for (int u = 0; u < DCOLS; ++u) {
@@ -790,7 +807,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
                 const int64_t nd = pis + ps[j] - (int64_t)__ldg(As + j);
                 d[j] = nd;
                 pred[j] = (int16_t)s;
-                const uint64_t k = ((uint64_t)nd << 24) | ((fl[j] & 2) ? 0u : (1u << 23)) | (uint32_t)j;
+                const uint64_t k = ((uint64_t)nd << kSH) | ((fl[j] & 2) ? 0u : kFreeBit) | (uint32_t)j;
                 best = k < best ? k : best;
             }
         }
@@ -798,12 +815,12 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
         int32_t jf;
         int64_t D;
         while (true) {
-            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
-            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t jm = (int32_t)(best & kIdxMask);
+            const int64_t dmin = (int64_t)(best >> kSH);
             if (fl[jm] & 2) { jf = jm; D = dmin; break; }
             const int32_t i = rocs[jm];
             if ((jm & (DTHREADS - 1)) == tid) fl[jm] |= 1;   // only the column's owner thread reads its flag
-            const int32_t* Ai = rowp(L, i);
+            const wt_t* Ai = rowp(L, i);
             // the whole row slice and a_i,jm in one batch of loads
             int32_t av[DCOLS];
 #pragma unroll
@@ -822,7 +839,7 @@ __global__ void __launch_bounds__(DTHREADS, 1) ssp_dense_kernel(Lvl L, int32_t n
                         int64_t dj = d[j];
                         const int64_t nd = base + ps[j] - (int64_t)av[u];
                         if (nd < dj) { dj = nd; d[j] = nd; pred[j] = (int16_t)i; }
-                        const uint64_t k = ((uint64_t)dj << 24) | ((f & 2) ? 0u : (1u << 23)) | (uint32_t)j;
+                        const uint64_t k = ((uint64_t)dj << kSH) | ((f & 2) ? 0u : kFreeBit) | (uint32_t)j;
                         best = k < best ? k : best;
                     }
                 }
@@ -901,7 +918,7 @@ __device__ __forceinline__ uint64_t cluster_min_fetch(uint64_t v, CShared& S, in
         if (lane_id() == 0) {
             S.bkey[par] = x;
             if (x != kNoKey) {
-                const int32_t j = (int32_t)(x & 0x7FFFFFu);
+                const int32_t j = (int32_t)(x & kIdxMask);
                 const int owner = j / mc;
                 S.bown[par] = cluster.map_shared_rank(rocs, owner)[j - owner * mc];
                 S.bprice[par] = cluster.map_shared_rank(ps, owner)[j - owner * mc];
@@ -1021,7 +1038,7 @@ ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
     __syncthreads();
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = rowp(L, s);
+        const wt_t* As = rowp(L, s);
         // one reduction finds both the source's profit (the largest a_sj - p_j)
         // and the first pop (that column, at distance 0; free columns first)
         uint64_t vmin = kNoKey;
@@ -1035,15 +1052,15 @@ ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
                 rocs[jj] = r;
                 fl[jj] = 0;
                 const int64_t v = pj - (int64_t)__ldg(As + c0 + jj);   // = -(a_sj - p_j)
-                const uint64_t k = ((uint64_t)(v + kDistLim) << 24) | (r < 0 ? 0u : (1u << 23)) | (uint32_t)(c0 + jj);
+                const uint64_t k = ((uint64_t)(v + kDistLim) << kSH) | (r < 0 ? 0u : kFreeBit) | (uint32_t)(c0 + jj);
                 vmin = k < vmin ? k : vmin;
             }
         }
         int32_t i;
         int64_t pjm;
         const uint64_t k0 = cluster_min_fetch<CLS>(vmin, S, par, cluster, mc, rocs, ps, i, pjm);
-        const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
-        uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
+        const int64_t pis = -((int64_t)(k0 >> kSH) - kDistLim);
+        uint64_t best = k0 & kLowMask;   // distance 0, same column and free bit
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * NT;
@@ -1057,14 +1074,14 @@ ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
         int32_t pops = 0;
         bool abandon = false;
         while (true) {
-            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
-            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t jm = (int32_t)(best & kIdxMask);
+            const int64_t dmin = (int64_t)(best >> kSH);
             if (i < 0) { jf = jm; D = dmin; break; }
             // coarse levels: a search past the pop limit is abandoned (row stays free)
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             if (jm >= c0 && jm < c0 + nloc && ((jm - c0) & (NT - 1)) == tid) fl[jm - c0] |= 1;
-            const int32_t* Ai = rowp(L, i);
-            int32_t av[CC];
+            const wt_t* Ai = rowp(L, i);
+            wt_t av[CC];
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * NT;
@@ -1079,7 +1096,7 @@ ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
                     int64_t dj = d[jj];
                     const int64_t nd = base + ps[jj] - (int64_t)av[u];
                     if (nd < dj) { dj = nd; d[jj] = nd; pred[jj] = i; }
-                    const uint64_t k = ((uint64_t)dj << 24) | (rocs[jj] < 0 ? 0u : (1u << 23)) | (uint32_t)(c0 + jj);
+                    const uint64_t k = ((uint64_t)dj << kSH) | (rocs[jj] < 0 ? 0u : kFreeBit) | (uint32_t)(c0 + jj);
                     best = k < best ? k : best;
                 }
             }
@@ -1119,11 +1136,11 @@ ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
 //
 // Thread t of CTA r owns columns c0 + t + u * NT (u < CC) for the whole
 // search, so their state never needs shared memory:
-//   kd[u] = (d_j << 24) | low_j           tentative distance as a sort key
-//   pk[u] = (p_j << 24) | low_j           price (constant during a search)
+//   kd[u] = (d_j << kSH) | low_j           tentative distance as a sort key
+//   pk[u] = (p_j << kSH) | low_j           price (constant during a search)
 //   low_j = (owned ? 1 << 23 : 0) | j     free columns first on ties, then lowest j
 // and relaxing row i at base distance b is one 64-bit add-subtract-compare:
-//   nk = (b << 24) + pk[u] - (a_ij << 24) = ((b + p_j - a_ij) << 24) | low_j.
+//   nk = (b << kSH) + pk[u] - (a_ij << kSH) = ((b + p_j - a_ij) << kSH) | low_j.
 // A popped column gets bit 63 in both words: its nk then carries bit 63 and is
 // never below kd (nd >= the popped distance), and it drops out of the minimum.
 // Only the predecessor row stays in shared memory (the augmenting-path walk
@@ -1149,7 +1166,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     int32_t* pred = rocr + ((m + 1) & ~1);                                    // [mc] predecessor rows (local)
     // two row-slice buffers for the runner-up prefetch (TMA bulk copies)
     const int32_t slot_words = ((mc + 8 + 3) & ~3);
-    int32_t* rowbuf = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(pred + mc) + 127) & ~(uintptr_t)127);
+    wt_t* rowbuf = reinterpret_cast<wt_t*>((reinterpret_cast<uintptr_t>(pred + mc) + 127) & ~(uintptr_t)127);
     __shared__ __align__(8) uint64_t pfbar[2];
     __shared__ int32_t pfrow[2], pfshift[2];
     __shared__ uint32_t pfpar[2];
@@ -1176,14 +1193,14 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     cluster.sync();
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = rowp(L, s);
+        const wt_t* As = rowp(L, s);
         for (int32_t j = tid; j < m; j += NT) {
             psr[j] = __ldcg(L.p + j);
             rocr[j] = __ldcg(L.roc + j);
         }
         __syncthreads();
         uint64_t kd[CC], pk[CC];
-        int32_t as[CC];
+        wt_t as[CC];
         // one reduction finds the source's profit (the largest a_sj - p_j) and
         // the first pop (that column at distance 0; free columns first)
         uint64_t vmin = kNoKey;
@@ -1199,9 +1216,9 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                 const int32_t j = c0 + jj;
                 const int64_t pj = psr[j];
                 if (pj < 0 || pj >= kDistLim) atomicOr(&L.cnt->errors, kErrDist);
-                const uint64_t low = (rocr[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
-                pk[u] = ((uint64_t)pj << 24) | low;
-                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << 24) | low;
+                const uint64_t low = (rocr[j] < 0 ? 0u : kFreeBit) | (uint32_t)j;
+                pk[u] = ((uint64_t)pj << kSH) | low;
+                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << kSH) | low;
                 vmin = k < vmin ? k : vmin;
                 pred[jj] = s;
             } else {
@@ -1209,27 +1226,27 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             }
         }
         const uint64_t k0 = cluster_min_push<CLS, NT / 32>(vmin, S, P, par, ph, rank, cand2);
-        const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
+        const int64_t pis = -((int64_t)(k0 >> kSH) - kDistLim);
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * NT;
-            kd[u] = jj < nloc ? (((uint64_t)pis << 24) + pk[u] - ((uint64_t)(uint32_t)as[u] << 24)) : kNoKey;
+            kd[u] = jj < nloc ? (((uint64_t)pis << kSH) + pk[u] - ((uint64_t)as[u] << kSH)) : kNoKey;
         }
-        uint64_t best = k0 & 0xFFFFFFull;   // distance 0, same column and free bit
+        uint64_t best = k0 & kLowMask;   // distance 0, same column and free bit
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
         bool abandon = false;
         while (true) {
-            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
-            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t jm = (int32_t)(best & kIdxMask);
+            const int64_t dmin = (int64_t)(best >> kSH);
             const int32_t i = rocr[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             const long long tA = tm ? clock64() : 0;
-            const int32_t* Ai = rowp(L, i);
+            const wt_t* Ai = rowp(L, i);
             const int64_t aim = (int64_t)__ldg(Ai + jm);
-            int32_t av[CC];
+            wt_t av[CC];
             if (pf && pfrow[cur] == i) {
                 // the runner-up of the previous step: its slice is (being) copied into smem
                 const uint32_t bar = smem_u32(&pfbar[cur]), parity = pfpar[cur];
@@ -1237,7 +1254,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                 while (!done)
                     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                                  : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-                const int32_t* rb = rowbuf + cur * slot_words + pfshift[cur];
+                const wt_t* rb = rowbuf + cur * slot_words + pfshift[cur];
 #pragma unroll
                 for (int u = 0; u < CC; ++u) {
                     const int32_t jj = tid + u * NT;
@@ -1257,7 +1274,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                 const uint64_t k2 = wmin64(cand2);
                 const int nb = cur ^ 1;
                 if (tid == 0 && k2 != kNoKey && nloc > 0) {
-                    const int32_t i2 = rocr[k2 & 0x7FFFFFu];
+                    const int32_t i2 = rocr[k2 & kIdxMask];
                     if (i2 >= 0 && i2 != pfrow[nb]) {
                         const uint32_t bar = smem_u32(&pfbar[nb]);
                         if (pfcount[nb] > 0) {
@@ -1268,7 +1285,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                                 asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                                              : "=r"(done) : "r"(bar), "r"(parity) : "memory");
                         }
-                        const int32_t* src = rowp(L, i2) + c0;
+                        const wt_t* src = rowp(L, i2) + c0;
                         const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
                         const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
                         const uint32_t bytes = (uint32_t)(a1 - a0);
@@ -1279,7 +1296,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                         pfpar[nb] = pfcount[nb] & 1u;
                         ++pfcount[nb];
                         pfrow[nb] = i2;
-                        pfshift[nb] = (int32_t)((reinterpret_cast<uintptr_t>(src) - a0) >> 2);
+                        pfshift[nb] = (int32_t)((reinterpret_cast<uintptr_t>(src) - a0) / sizeof(wt_t));
                     }
                 }
             }
@@ -1289,11 +1306,11 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                 for (int u = 0; u < CC; ++u)
                     if (jm - c0 == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
             }
-            const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << 24;
+            const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << kSH;
             best = kNoKey;
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const uint64_t nk = base + pk[u] - ((uint64_t)(uint32_t)av[u] << 24);
+                const uint64_t nk = base + pk[u] - ((uint64_t)av[u] << kSH);
                 if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
                 best = kd[u] < best ? kd[u] : best;
             }
@@ -1314,7 +1331,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * NT;
                 if (jj < nloc && (kd[u] & kTop)) {
-                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> 24), dj = (int64_t)((kd[u] & ~kTop) >> 24);
+                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> kSH), dj = (int64_t)((kd[u] & ~kTop) >> kSH);
                     L.p[c0 + jj] = pj + (D - dj);
                 }
             }
@@ -1357,7 +1374,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
 // in every CTA (m > CL * 2048: the 10k x 40k rounds of config 5).  Each
 // thread keeps its columns' keys, prices and owners in registers; a warp's
 // minimum travels with its column's owner row and price packed into a second
-// word (price << 24 | owner + 1), pushed as one 16-byte st.async, so the
+// word (price << kSH | owner + 1), pushed as one 16-byte st.async, so the
 // winner's row and price arrive with the key -- no replicated tables, no
 // DSMEM fetch after the exchange.
 template <int CLS, int NW>
@@ -1454,7 +1471,7 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
     cluster.sync();
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = rowp(L, s);
+        const wt_t* As = rowp(L, s);
         uint64_t kd[CC], pk[CC];
         int32_t own[CC], as[CC];
 #pragma unroll
@@ -1471,38 +1488,38 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                 const int32_t j = c0 + jj;
                 const int64_t pj = __ldcg(L.p + j);
                 if (pj < 0 || pj >= kDistLim) atomicOr(&L.cnt->errors, kErrDist);
-                const uint64_t low = (own[u] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
-                pk[u] = ((uint64_t)pj << 24) | low;
-                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << 24) | low;
-                if (k < vmin) { vmin = k; vpay = ((uint64_t)pj << 24) | (uint32_t)(own[u] + 1); }
+                const uint64_t low = (own[u] < 0 ? 0u : kFreeBit) | (uint32_t)j;
+                pk[u] = ((uint64_t)pj << kSH) | low;
+                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << kSH) | low;
+                if (k < vmin) { vmin = k; vpay = ((uint64_t)pj << kSH) | (uint32_t)(own[u] + 1); }
                 pred[jj] = s;
             } else {
                 pk[u] = kTop;
             }
         }
         const ulonglong2 r0 = cluster_min_push2<CLS, NW>(vmin, vpay, bres, P, par, ph, rank);
-        const int64_t pis = -((int64_t)(r0.x >> 24) - kDistLim);
+        const int64_t pis = -((int64_t)(r0.x >> kSH) - kDistLim);
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
             const int32_t jj = tid + u * NT;
-            kd[u] = jj < nloc ? (((uint64_t)pis << 24) + pk[u] - ((uint64_t)(uint32_t)as[u] << 24)) : kNoKey;
+            kd[u] = jj < nloc ? (((uint64_t)pis << kSH) + pk[u] - ((uint64_t)as[u] << kSH)) : kNoKey;
         }
-        uint64_t best = r0.x & 0xFFFFFFull;
+        uint64_t best = r0.x & kLowMask;
         uint64_t bpay = r0.y;
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
         bool abandon = false;
         while (true) {
-            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
-            const int64_t dmin = (int64_t)(best >> 24);
-            const int32_t i = (int32_t)(bpay & 0xFFFFFFu) - 1;
-            const int64_t pjm = (int64_t)(bpay >> 24);
+            const int32_t jm = (int32_t)(best & kIdxMask);
+            const int64_t dmin = (int64_t)(best >> kSH);
+            const int32_t i = (int32_t)(bpay & kLowMask) - 1;
+            const int64_t pjm = (int64_t)(bpay >> kSH);
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             const long long tA = tm ? clock64() : 0;
-            const int32_t* Ai = rowp(L, i);
-            int32_t av[CC];
+            const wt_t* Ai = rowp(L, i);
+            wt_t av[CC];
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * NT;
@@ -1514,14 +1531,14 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                 for (int u = 0; u < CC; ++u)
                     if (jm - c0 == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
             }
-            const uint64_t base = (uint64_t)(dmin + aim - pjm) << 24;
+            const uint64_t base = (uint64_t)(dmin + aim - pjm) << kSH;
             best = kNoKey;
             uint64_t pay = 0;
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const uint64_t nk = base + pk[u] - ((uint64_t)(uint32_t)av[u] << 24);
+                const uint64_t nk = base + pk[u] - ((uint64_t)av[u] << kSH);
                 if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
-                if (kd[u] < best) { best = kd[u]; pay = ((pk[u] & ~kTop) & ~0xFFFFFFull) | (uint32_t)(own[u] + 1); }
+                if (kd[u] < best) { best = kd[u]; pay = ((pk[u] & ~kTop) & ~kLowMask) | (uint32_t)(own[u] + 1); }
             }
             const long long tB = tm ? clock64() : 0;
             const ulonglong2 r = cluster_min_push2<CLS, NW>(best, pay, bres, P, par, ph, rank);
@@ -1540,7 +1557,7 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
             for (int u = 0; u < CC; ++u) {
                 const int32_t jj = tid + u * NT;
                 if (jj < nloc && (kd[u] & kTop)) {
-                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> 24), dj = (int64_t)((kd[u] & ~kTop) >> 24);
+                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> kSH), dj = (int64_t)((kd[u] & ~kTop) >> kSH);
                     L.p[c0 + jj] = pj + (D - dj);
                 }
             }
@@ -1604,14 +1621,14 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
     };
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
-        const int32_t* As = rowp(L, s);
+        const wt_t* As = rowp(L, s);
         for (int32_t j = tid; j < m; j += NT) {
             psr[j] = __ldcg(L.p + j);
             rocr[j] = __ldcg(L.roc + j);
         }
         __syncthreads();
         uint64_t kd[CC], pk[CC];
-        int32_t as[CC];
+        wt_t as[CC];
         uint64_t vmin = kNoKey;
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
@@ -1624,9 +1641,9 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
             if (j < m) {
                 const int64_t pj = psr[j];
                 if (pj < 0 || pj >= kDistLim) atomicOr(&L.cnt->errors, kErrDist);
-                const uint64_t low = (rocr[j] < 0 ? 0u : (1u << 23)) | (uint32_t)j;
-                pk[u] = ((uint64_t)pj << 24) | low;
-                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << 24) | low;
+                const uint64_t low = (rocr[j] < 0 ? 0u : kFreeBit) | (uint32_t)j;
+                pk[u] = ((uint64_t)pj << kSH) | low;
+                const uint64_t k = ((uint64_t)(pj - (int64_t)as[u] + kDistLim) << kSH) | low;
                 vmin = k < vmin ? k : vmin;
                 pred[j] = s;
             } else {
@@ -1634,26 +1651,26 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
             }
         }
         const uint64_t k0 = block_min(vmin);
-        const int64_t pis = -((int64_t)(k0 >> 24) - kDistLim);
+        const int64_t pis = -((int64_t)(k0 >> kSH) - kDistLim);
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
             const int32_t j = tid + u * NT;
-            kd[u] = j < m ? (((uint64_t)pis << 24) + pk[u] - ((uint64_t)(uint32_t)as[u] << 24)) : kNoKey;
+            kd[u] = j < m ? (((uint64_t)pis << kSH) + pk[u] - ((uint64_t)as[u] << kSH)) : kNoKey;
         }
-        uint64_t best = k0 & 0xFFFFFFull;
+        uint64_t best = k0 & kLowMask;
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
         bool abandon = false;
         while (true) {
-            const int32_t jm = (int32_t)(best & 0x7FFFFFu);
-            const int64_t dmin = (int64_t)(best >> 24);
+            const int32_t jm = (int32_t)(best & kIdxMask);
+            const int64_t dmin = (int64_t)(best >> kSH);
             const int32_t i = rocr[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             const long long tA = tm ? clock64() : 0;
-            const int32_t* Ai = rowp(L, i);
-            int32_t av[CC];
+            const wt_t* Ai = rowp(L, i);
+            wt_t av[CC];
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
                 const int32_t j = tid + u * NT;
@@ -1663,11 +1680,11 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
 #pragma unroll
             for (int u = 0; u < CC; ++u)
                 if (jm == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
-            const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << 24;
+            const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << kSH;
             best = kNoKey;
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
-                const uint64_t nk = base + pk[u] - ((uint64_t)(uint32_t)av[u] << 24);
+                const uint64_t nk = base + pk[u] - ((uint64_t)av[u] << kSH);
                 if (tid + u * NT < m && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
                 best = kd[u] < best ? kd[u] : best;
             }
@@ -1686,7 +1703,7 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
             for (int u = 0; u < CC; ++u) {
                 const int32_t j = tid + u * NT;
                 if (j < m && (kd[u] & kTop)) {
-                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> 24), dj = (int64_t)((kd[u] & ~kTop) >> 24);
+                    const int64_t pj = (int64_t)((pk[u] & ~kTop) >> kSH), dj = (int64_t)((kd[u] & ~kTop) >> kSH);
                     L.p[j] = pj + (D - dj);
                 }
             }
@@ -1716,21 +1733,21 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
 // ---------------------------------------------------------------------------
 
 // A_l[r][c] = W[rows[r]][cols[c]] (rows >= N are the zero padding rows)
-__global__ void gather_kernel(const int32_t* W, int64_t ldw, int32_t N, const int32_t* rows, const int32_t* cols,
-                              int32_t m, int32_t* out) {
+__global__ void gather_kernel(const wt_t* W, int64_t ldw, int32_t N, const int32_t* rows, const int32_t* cols,
+                              int32_t m, wt_t* out) {
     for (int32_t r = blockIdx.x; r < m; r += gridDim.x) {
         const int32_t ri = rows[r];
         if (ri >= N) {
             for (int32_t c = threadIdx.x; c < m; c += blockDim.x) out[(int64_t)r * m + c] = 0;
             continue;
         }
-        const int32_t* Wr = W + (int64_t)ri * ldw;
+        const wt_t* Wr = W + (int64_t)ri * ldw;
         for (int32_t c = threadIdx.x; c < m; c += blockDim.x) out[(int64_t)r * m + c] = __ldg(Wr + cols[c]);
     }
 }
 
 // base level: p_j = max_i a_ij (rows >= nreal are zero)
-__global__ void colmax_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, int64_t* p) {
+__global__ void colmax_kernel(const wt_t* A, int64_t lda, int32_t nreal, int32_t m, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     int64_t b = nreal < m ? 0 : INT64_MIN;
@@ -1763,7 +1780,7 @@ __global__ void warm_pmin_kernel(const int64_t* pin, int32_t m, unsigned long lo
     if (lane_id() == 0 && b != INT64_MAX) atomicMin(reinterpret_cast<long long*>(pmin), (long long)b);
 }
 
-__global__ void warm_profit_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin,
+__global__ void warm_profit_kernel(const wt_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin,
                                    int64_t* pi) {
     const int32_t k = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     if (k >= nreal) return;
@@ -1779,7 +1796,7 @@ __global__ void warm_profit_kernel(const int32_t* A, int64_t lda, int32_t nreal,
     if (lane_id() == 0) pi[k] = b;
 }
 
-__global__ void warm_price_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin,
+__global__ void warm_price_kernel(const wt_t* A, int64_t lda, int32_t nreal, int32_t m, const int64_t* pin,
                                   const int64_t* pi, const unsigned long long* pminp, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
@@ -1795,7 +1812,7 @@ __global__ void warm_price_kernel(const int32_t* A, int64_t lda, int32_t nreal, 
 
 // keep the previous pairs that are still tight; the unmatched rows form the
 // search list (cnt->qhead counts them)
-__global__ void warm_match_kernel(const int32_t* A, int64_t lda, int32_t nreal, int32_t m, const int32_t* wcol,
+__global__ void warm_match_kernel(const wt_t* A, int64_t lda, int32_t nreal, int32_t m, const int32_t* wcol,
                                   const int64_t* pi, const int64_t* p, int32_t* cor, int32_t* roc) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nreal) return;
@@ -1836,7 +1853,7 @@ __global__ void split_rows_kernel(int32_t n, const int32_t* in, int32_t plo, int
 // pi_k of a solved level: a_k,cor(k) - p_cor(k) for matched rows; rows a
 // coarse level left unmatched (its long searches are skipped) take the
 // dual-feasible max_j (a_kj - p_j).  One warp per row.
-__global__ void profit_kernel(const int32_t* A, int64_t lda, int32_t m, const int32_t* cor, const int64_t* p,
+__global__ void profit_kernel(const wt_t* A, int64_t lda, int32_t m, const int32_t* cor, const int64_t* p,
                               int64_t* pi) {
     const int32_t k = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     if (k >= m) return;
@@ -1857,7 +1874,7 @@ __global__ void profit_kernel(const int32_t* A, int64_t lda, int32_t m, const in
 // c-transform: p_j = max_k (A[sub[k]][j] - pi_k) over the coarse rows k.
 // blockIdx.y takes one chunk of the coarse rows; partial maxima meet in an
 // atomicMax (p pre-filled with INT64_MIN).
-__global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t nreal, const int32_t* zrow, int32_t m,
+__global__ void ctransform_kernel(const wt_t* A, int64_t lda, int32_t nreal, const wt_t* zrow, int32_t m,
                                   const int32_t* sub, const int64_t* pi, int32_t mc, int32_t chunk, int64_t* p) {
     const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
@@ -1869,7 +1886,7 @@ __global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t nreal, 
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int32_t r = __ldg(sub + k + u);
-            const int32_t* Ar = r < nreal ? A + (int64_t)r * lda : zrow;
+            const wt_t* Ar = r < nreal ? A + (int64_t)r * lda : zrow;
             v[u] = (int64_t)__ldg(Ar + j) - __ldg(pi + k + u);
         }
 #pragma unroll
@@ -1877,7 +1894,7 @@ __global__ void ctransform_kernel(const int32_t* A, int64_t lda, int32_t nreal, 
     }
     for (; k < k1; ++k) {
         const int32_t r = __ldg(sub + k);
-        const int32_t* Ar = r < nreal ? A + (int64_t)r * lda : zrow;
+        const wt_t* Ar = r < nreal ? A + (int64_t)r * lda : zrow;
         const int64_t v = (int64_t)__ldg(Ar + j) - __ldg(pi + k);
         b = v > b ? v : b;
     }
@@ -1901,7 +1918,7 @@ __global__ void init_level_kernel(int32_t m, int32_t* cor, int32_t* roc, int32_t
 }
 
 // finished level 0: col_out (original indexing) and the total
-__global__ void finish_kernel(const int32_t* W, int64_t ldw, int32_t n, const int32_t* cor, int32_t* col_out,
+__global__ void finish_kernel(const wt_t* W, int64_t ldw, int32_t n, const int32_t* cor, int32_t* col_out,
                               unsigned long long* total) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     long long q = 0;
@@ -1918,11 +1935,11 @@ __global__ void finish_kernel(const int32_t* W, int64_t ldw, int32_t n, const in
 // dense certificate (tests / MUX_SSP_CHECK): bad[0] unmatched rows, bad[1]
 // row/column inconsistency, bad[2] dual violations pi_i + p_j < a_ij,
 // bad[3] = first violating (i << 32 | j)
-__global__ void check_kernel(const int32_t* A, int64_t lda, int32_t nreal, const int32_t* zrow, int32_t m,
+__global__ void check_kernel(const wt_t* A, int64_t lda, int32_t nreal, const wt_t* zrow, int32_t m,
                              const int32_t* cor, const int32_t* roc, const int64_t* p, unsigned long long* bad) {
     const int32_t i = blockIdx.x;
     if (i >= m) return;
-    const int32_t* Ai = i < nreal ? A + (int64_t)i * lda : zrow;
+    const wt_t* Ai = i < nreal ? A + (int64_t)i * lda : zrow;
     const int32_t j0 = cor[i];
     if (j0 < 0) { if (threadIdx.x == 0) atomicAdd(bad, 1ull); return; }
     if (threadIdx.x == 0 && roc[j0] != i) atomicAdd(bad + 1, 1ull);
@@ -1937,7 +1954,7 @@ __global__ void check_kernel(const int32_t* A, int64_t lda, int32_t nreal, const
 }
 
 // row / column sums: generic ordering keys when the caller has none
-__global__ void rowsum_kernel(const int32_t* W, int64_t ldw, int32_t M, double* rs, double* cs) {
+__global__ void rowsum_kernel(const wt_t* W, int64_t ldw, int32_t M, double* rs, double* cs) {
     const int32_t i = blockIdx.x;
     double s = 0;
     for (int32_t j = threadIdx.x; j < M; j += blockDim.x) {
@@ -1949,11 +1966,17 @@ __global__ void rowsum_kernel(const int32_t* W, int64_t ldw, int32_t M, double* 
     if ((threadIdx.x & 31) == 0) atomicAdd(rs + i, s);
 }
 
-}  // namespace ssp
+}  // namespace ssp / ssp64
 }  // namespace mux
 
 using namespace mux;
+#ifndef MUX_SSP_W64
 using namespace mux::ssp;
+#define MUX_SSP_IMPL mux_ssp_impl
+#else
+using namespace mux::ssp64;
+#define MUX_SSP_IMPL mux_ssp_impl64
+#endif
 
 static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
@@ -1962,14 +1985,14 @@ static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 // price_out (device int64 [n], optional): optimal column prices (max form).
 // Solves the reference's square problem of size n = M: rows N..M-1 are the
 // zero padding rows (N <= M).
-int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
+int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t M, const double* rowkey,
                  const double* colkey, int32_t* col_out, int64_t* total_q, int64_t* price_out,
                  int32_t* cor_out, int32_t* roc_out, mux_stats_t* stats, cudaStream_t st, const int64_t* price_in,
                  const int32_t* warm_col) {
     const int32_t n = M;
     if (n <= 0 || N <= 0) { if (total_q) *total_q = 0; return MUX_OK; }
     if (N > M) { set_error("ssp: needs N <= M"); return MUX_EINVAL; }
-    if (n >= (1 << 23)) { set_error("ssp: problem too large"); return MUX_EINVAL; }
+    if (n >= (int32_t)kIdxMask - 128) { set_error("ssp: problem too large for its key format"); return MUX_EINVAL; }
     const Tuning& T = tuning();
     const bool verbose = T.verbose;
     const int fct = T.ssp_f;
@@ -2045,14 +2068,14 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     auto take = [&](size_t b) { size_t o = off; off += al256(b); return o; };
     const size_t o_cnt = take(sizeof(Cnt));
     const size_t o_tot = take(32);
-    const size_t o_zero = take(4ull * n + 64);
+    const size_t o_zero = take(sizeof(wt_t) * n + 64);
     std::vector<size_t> o_A(nl), o_p(nl), o_cor(nl), o_roc(nl), o_lock(nl), o_cj(nl), o_ca(nl), o_tau(nl), o_in(nl),
         o_re(nl), o_de(nl), o_tr(nl), o_pi(nl), o_sub(nl), o_rows(nl), o_cols(nl), o_rl(nl);
     for (int l = 0; l < nl; ++l) {
         const size_t m = (size_t)lv[l].m;
-        o_A[l] = l ? take(4 * m * m) : 0;
+        o_A[l] = l ? take(sizeof(wt_t) * m * m) : 0;
         o_p[l] = take(8 * m); o_cor[l] = take(4 * m); o_roc[l] = take(4 * m); o_lock[l] = take(4 * m);
-        o_cj[l] = take(4 * m * KC); o_ca[l] = take(4 * m * KC); o_tau[l] = take(8 * m);
+        o_cj[l] = take(4 * m * KC); o_ca[l] = take(sizeof(wt_t) * m * KC); o_tau[l] = take(8 * m);
         o_in[l] = take(4 * m); o_re[l] = take(4 * m); o_de[l] = take(4 * m); o_tr[l] = take(4 * m);
         o_pi[l] = take(8 * m);
         o_sub[l] = take(4 * (lv[l].sub.size() + 1));
@@ -2067,7 +2090,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
     MUX_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(Cnt), st));
     MUX_CUDA_TRY(cudaMemsetAsync(B + o_tot, 0, 8, st));
     MUX_CUDA_TRY(cudaMemsetAsync(B + o_zero, 0, 4ull * n + 64, st));
-    const int32_t* zrow = reinterpret_cast<const int32_t*>(B + o_zero);
+    const wt_t* zrow = reinterpret_cast<const wt_t*>(B + o_zero);
 
     // upload index lists and gather the coarse matrices
     for (int l = 1; l < nl; ++l) {
@@ -2075,7 +2098,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         MUX_CUDA_TRY(cudaMemcpyAsync(B + o_cols[l], lv[l].cols.data(), 4ull * lv[l].m, cudaMemcpyHostToDevice, st));
         gather_kernel<<<std::min<int32_t>(lv[l].m, 4096), 256, 0, st>>>(
             W, ldw, N, reinterpret_cast<int32_t*>(B + o_rows[l]), reinterpret_cast<int32_t*>(B + o_cols[l]), lv[l].m,
-            reinterpret_cast<int32_t*>(B + o_A[l]));
+            reinterpret_cast<wt_t*>(B + o_A[l]));
     }
     for (int l = 0; l + 1 < nl; ++l)
         MUX_CUDA_TRY(cudaMemcpyAsync(B + o_sub[l], lv[l].sub.data(), 4ull * lv[l].sub.size(), cudaMemcpyHostToDevice, st));
@@ -2130,7 +2153,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         auto tl = std::chrono::steady_clock::now();
         const int32_t m = lv[l].m;
         Lvl L{};
-        L.A = l ? reinterpret_cast<const int32_t*>(B + o_A[l]) : W;
+        L.A = l ? reinterpret_cast<const wt_t*>(B + o_A[l]) : W;
         L.lda = l ? m : ldw;
         L.m = m;
         L.nreal = l ? m : N;
@@ -2140,7 +2163,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
         L.roc = reinterpret_cast<int32_t*>(B + o_roc[l]);
         L.lock = reinterpret_cast<int32_t*>(B + o_lock[l]);
         L.cj = reinterpret_cast<int32_t*>(B + o_cj[l]);
-        L.ca = reinterpret_cast<int32_t*>(B + o_ca[l]);
+        L.ca = reinterpret_cast<wt_t*>(B + o_ca[l]);
         L.tau = reinterpret_cast<int64_t*>(B + o_tau[l]);
         L.retry = reinterpret_cast<int32_t*>(B + o_re[l]);
         L.defer = reinterpret_cast<int32_t*>(B + o_de[l]);
@@ -2185,7 +2208,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const int32_t mc = lv[l + 1].m;
             int64_t* pic = reinterpret_cast<int64_t*>(B + o_pi[l + 1]);
             profit_kernel<<<(unsigned)(((int64_t)mc * 32 + 255) / 256), 256, 0, st>>>(
-                reinterpret_cast<const int32_t*>(B + o_A[l + 1]), mc, mc, reinterpret_cast<int32_t*>(B + o_cor[l + 1]),
+                reinterpret_cast<const wt_t*>(B + o_A[l + 1]), mc, mc, reinterpret_cast<int32_t*>(B + o_cor[l + 1]),
                 reinterpret_cast<int64_t*>(B + o_p[l + 1]), pic);
             fill_i64_kernel<<<g1, 256, 0, st>>>(L.p, m, INT64_MIN);
             const int32_t ksplit = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * 8 / g1, mc / 64));
@@ -2246,7 +2269,7 @@ int mux_ssp_impl(mux_ctx_t* ctx, const int32_t* W, int64_t ldw, int32_t N, int32
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
             // register-key kernel: 12 m replicated + 4 bytes per local column + two row-slice buffers
-            const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * 4 * ((mcl + 8 + 3) & ~3) + 64;
+            const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * sizeof(wt_t) * ((mcl + 8 + 3) & ~3) + 64;
             const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8 && T.ssp_rslice != 2;
             const bool slice_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
             // single SM for levels up to T.ssp_one columns: one barrier per pop, no DSMEM

@@ -55,11 +55,11 @@ def max_qbits(n: int, cap: int = 30) -> int:
 
 def round_qbits(n: int) -> int:
     """Quantisation of a scheduling round: the exact-parity mode (int64
-    weights, up to 40 bits) where the bid packing leaves
-    at least 32 bits, else 30-bit int32 weights (large rounds, where int64
-    rows would no longer fit the auction's shared-memory staging)."""
-    q = max_qbits(n, cap=40)
-    return q if (q >= 32 and n <= 6144) else min(q, 30)
+    weights, 40 bits) for rounds up to 6,144 on the larger
+    side, else 30-bit int32 weights (the int64 matrix of a large round doubles
+    the bytes every long-path pop loads).  Both run on the multilevel
+    shortest-path solver (csrc/ssp.cu, csrc/ssp_w64.cu)."""
+    return 40 if n <= 6144 else 30
 
 
 def match_dense(Wq, n=None, m=None, stats=False):

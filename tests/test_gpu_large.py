@@ -122,16 +122,18 @@ def _f64_total(W, col):
     return float(sum(W[i, j] for i, j in enumerate(col) if j >= 0))
 
 
-def test_int64_round_total_matches_reference_algorithm(cuda):
-    """schedule()'s exact-parity quantisation at 4k (round_qbits: 35-bit int64
-    weights, the epsilon-scaling auction): the optimal integer total equals the
-    reference algorithm's on the same integers (the oracle's int64 Hungarian,
-    large_q35 golden)."""
+@pytest.mark.parametrize("q", [35, 40])
+def test_int64_round_total_matches_reference_algorithm(cuda, certified, q):
+    """Int64 weights at 4k (40 bits = schedule()'s exact-parity quantisation,
+    round_qbits; the multilevel solver compiled for int64, csrc/ssp_w64.cu):
+    the optimal integer total equals the reference algorithm's on the same
+    integers (the oracle's int64 Hungarian, large_q35 / large_q40 goldens)."""
     from paper_2303_13803_b200.matching import round_qbits
-    g = _load(os.path.join(GOLD, "large_q35_4000x4000_s0.json"))
-    assert round_qbits(max(g["n"], g["m"])) == g["qbits"] == 35
-    _cl, W, col, total, _st = _round(cuda, g["n"], g["m"], g["seed"], g["qbits"])
+    g = _load(os.path.join(GOLD, f"large_q{q}_4000x4000_s0.json"))
+    assert round_qbits(max(g["n"], g["m"])) == 40
+    _cl, W, col, total, st = _round(cuda, g["n"], g["m"], g["seed"], g["qbits"])
     assert total == g["total_q"]
+    assert st["levels"] > 1          # the multilevel solver, not the auction
 
 
 def test_unique_float64_optimum_needs_more_than_40_bits(cuda):
@@ -139,8 +141,8 @@ def test_unique_float64_optimum_needs_more_than_40_bits(cuda):
     optimum of the 4k snapshot is certified unique, but only by ~1e-12
     margins: the reference algorithm itself on 35- and 40-bit integer
     weights lands on tied optima that differ from its float64 answer in 156
-    and 8 rows (goldens).  The GPU round at schedule()'s 35 bits is one of the
-    35-bit optima (same integer total, previous test) and stays within the
+    and 8 rows (goldens).  The GPU round at schedule()'s 40 bits is one of the
+    40-bit optima (same integer total, previous test) and stays within the
     tolerance; the rows it differs in are reported, not asserted."""
     from paper_2303_13803_b200.matching import round_qbits
     g, ref = _ref_col(F64_4K)
@@ -156,7 +158,7 @@ def test_unique_float64_optimum_needs_more_than_40_bits(cuda):
     gap = g["total_f64"] - _f64_total(Wf, col)
     assert -1e-9 <= gap <= g["n"] * 2.0 ** -20
     print(f"reference on 35 / 40 bits differs from its float64 optimum in {d35} / {d40} rows; "
-          f"GPU 35-bit round: {int(np.sum(col.astype(np.int64) != ref))} rows, float64 gap {gap:.3e}")
+          f"GPU 40-bit round: {int(np.sum(col.astype(np.int64) != ref))} rows, float64 gap {gap:.3e}")
 
 
 def test_schedule_drop_in_at_4k(cuda):

@@ -269,3 +269,48 @@ def test_tuning_knobs_are_gated_and_validated(cuda, monkeypatch):
     monkeypatch.delenv("MUX_SOLVER")
     with pytest.raises(nat.NativeError, match="MUX_SSP_F=99"):
         _match(Q)
+
+
+def _match64(Q, keys=None):
+    """_match for int64 weights (the solver compiled with 17-bit key indices)."""
+    import torch
+    from paper_2303_13803_b200 import _native as nat
+    n, m = Q.shape
+    ldw = max(2, (m + 1) // 2 * 2)
+    P = np.zeros((n, ldw), dtype=np.int64)
+    P[:, :m] = Q
+    Wq = torch.as_tensor(P, device="cuda")
+    col = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+    total = nat.ctypes.c_int64(0)
+    st = nat.MuxStats()
+    rp = cp = None
+    if keys is not None:
+        rk = torch.as_tensor(np.asarray(keys[0], dtype=np.float64), device="cuda")
+        ck = torch.as_tensor(np.asarray(keys[1], dtype=np.float64), device="cuda")
+        rp, cp = rk.data_ptr(), ck.data_ptr()
+    nat.check(nat.load().mux_match_keyed(nat.context(0), Wq.data_ptr(), nat.MUX_W_I64, n, m, ldw, rp, cp,
+                                         col.data_ptr(), 0, nat.ctypes.byref(total), nat.ctypes.byref(st),
+                                         nat.stream_ptr()))
+    return col[:n].cpu().numpy(), int(total.value), st.as_dict()
+
+
+@pytest.mark.parametrize("n,m,hi,seed", [(300, 300, 1 << 40, 0), (1000, 1000, 1 << 40, 1), (500, 1300, 1 << 38, 2),
+                                         (1200, 700, 1 << 40, 3), (800, 800, 5, 4)])
+def test_int64_weights_on_the_multilevel_solver(cuda, certified, n, m, hi, seed):
+    """Int64 weights (up to 40 bits, square and rectangular both ways, and
+    heavily tied) solved by the int64 build of the solver, vs scipy LSA."""
+    Q = np.random.default_rng(seed).integers(1, hi, size=(n, m)).astype(np.int64)
+    col, total, st = _match64(Q)
+    assert total == _lsa(Q)
+    assert st["levels"] >= 1                                 # the multilevel solver, not the auction
+    _check_assignment(Q, col, total)
+
+
+def test_int64_predictor_round_vs_oracle_hungarian(cuda, certified):
+    """40-bit predictor weights: the integer optimum equals the reference
+    algorithm's (the oracle's int64 Hungarian)."""
+    cl, Q = _pred_Q(900, 12, 40)
+    want, _ = matching_ref.max_weight_total_int(Q)
+    col, total, _st = _match64(Q, keys=(cl.x, cl.y))
+    assert total == want
+    _check_assignment(Q, col, total)
