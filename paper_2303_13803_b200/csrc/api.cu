@@ -64,7 +64,7 @@ const Tuning& tuning() {
         t.ssp_one = knob("MUX_SSP_ONE", t.ssp_one, 0, 10240, err);
         t.ssp_rslice = knob("MUX_SSP_RSLICE", 1, 0, 2, err);
         t.auc_theta = knob("MUX_THETA", t.auc_theta, 2, 64, err);
-        t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 16, err);
+        t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 1 << 20, err);   // clamped to the tail buffer inside
         t.auc_k = knob("MUX_K", t.auc_k, 1, 15, err);
         t.auc_cg_sync = knob("MUX_CG_SYNC", 1, 0, 1, err) == 1;
         t.auc_async_tail = knob("MUX_ASYNC_TAIL", -1, -1, 1, err);

@@ -67,7 +67,7 @@ struct Tuning {
     int ssp_rslice = 1;          // MUX_SSP_RSLICE [0, 2]: 0 = large levels on the shared-memory sliced kernel, 2 = every cluster level on it
     int ssp_one = 2560;          // MUX_SSP_ONE [0, 10240]: levels up to this size run long paths on one SM
     int auc_theta = 4;           // MUX_THETA [2, 64]: epsilon-scaling factor
-    int auc_tail = -1;           // MUX_TAIL [-1, 16]: unassigned count that ends the Jacobi rounds
+    int auc_tail = -1;           // MUX_TAIL [-1, 2^20]: unassigned count that ends the Jacobi rounds (clamped to 16)
     int auc_k = 15;              // MUX_K [1, 15]: cached candidates per bidder
     bool auc_cg_sync = true;     // MUX_CG_SYNC=0: custom grid barrier
     int auc_async_tail = -1;     // MUX_ASYNC_TAIL [-1, 1]: concurrent tail chains (-1 = n >= 512)

@@ -2089,7 +2089,7 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     Cnt* cnt = reinterpret_cast<Cnt*>(B + o_cnt);
     MUX_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(Cnt), st));
     MUX_CUDA_TRY(cudaMemsetAsync(B + o_tot, 0, 8, st));
-    MUX_CUDA_TRY(cudaMemsetAsync(B + o_zero, 0, 4ull * n + 64, st));
+    MUX_CUDA_TRY(cudaMemsetAsync(B + o_zero, 0, sizeof(wt_t) * n + 64, st));
     const wt_t* zrow = reinterpret_cast<const wt_t*>(B + o_zero);
 
     // upload index lists and gather the coarse matrices
