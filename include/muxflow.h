@@ -90,10 +90,10 @@ typedef struct {
     int64_t tail_bids;       /* bids made in single-CTA tail mode          */
     int64_t total_q;         /* optimal total, in quantised units          */
     double  ms_score;        /* device time of the scoring kernel(s)       */
-    double  ms_match;        /* device time of the auction                 */
+    double  ms_match;        /* wall time of the matching (solve + canonicalisation) */
     int64_t launches;        /* kernel launches issued by the call         */
     double  ms_tail;         /* device time in single-CTA tail mode        */
-    double  ms_kernel;       /* device time of the auction kernel (globaltimer) */
+    double  ms_kernel;       /* solver time (multilevel solver: as ms_match; auction: kernel time) */
     int64_t cache_hits;      /* bids served from the candidate cache       */
     double  ms_canon;        /* host time of the tie canonicalisation (incl. its kernels) */
     int64_t canon_searches;  /* alternating-path searches it ran           */
@@ -159,8 +159,10 @@ int mux_score_mlp(mux_ctx_t* ctx, const mux_mlp_t* mlp,
  * (replaces max_weight_matching, matching.py:148-208, including its tie
  * canonicalisation, matching.py:173-199).  Wq_dev: row-major [n][ldw] of wtype MUX_W_I32 or
  * MUX_W_I64 (0 = missing edge).  Solves the reference's zero-padded square
- * problem exactly (epsilon-scaling auction to epsilon = 1 on weights scaled by
- * max(n, m) + 1).  col_of_row_out: int32 [n], -1 when the row is unmatched or
+ * problem exactly: the multilevel successive-shortest-path solver (csrc/ssp.cu;
+ * int64 weights up to 44 bits with max(n, m) < 60,000, csrc/ssp_w64.cu), the
+ * epsilon-scaling auction beyond that or under MUX_TUNING=1 MUX_SOLVER=auction.
+ * col_of_row_out: int32 [n], -1 when the row is unmatched or
  * matched through a zero-weight / padding edge (the reference never emits
  * those, matching.py:201-208); may be a host or device pointer
  * (`out_on_host`).  *total_q receives the optimal total in quantised units.
@@ -186,13 +188,13 @@ int mux_match_keyed(mux_ctx_t* ctx, const void* Wq_dev, int wtype,
 /*
  * One fused scheduling round from HOST feature arrays (the call the
  * reference's `_matching_policy_schedule` makes per round, scheduler.py:143-194):
- * H2D copy of (x, share, y), exact scoring into quantised weights, auction,
+ * H2D copy of (x, share, y), exact scoring into quantised weights, the solve,
  * D2H copy of col_of_row.  Rows with share <= 0 must already be filtered by
  * the caller (scheduler.py:164-165), as must inadmissible columns
  * (scheduler.py:138-140).  qbits in [1, 52]: weights rint(w * 2^qbits) are
  * int32 up to 30 bits and int64 above (the exact-parity mode that schedule()
- * uses for small rounds); the auction's bid packing bounds qbits by about
- * 60 - 2 log2(max(n, m)).
+ * uses for rounds up to 6,144: 40 bits); the int64 solver's keys bound qbits
+ * by 44, the auction's bid packing by about 60 - 2 log2(max(n, m)).
  */
 int mux_round(mux_ctx_t* ctx, const mux_table_t* table,
               const double* x_host, const double* share_host, int64_t n,
