@@ -20,7 +20,11 @@
 
 constexpr int kMaxG = 8;
 
-struct Boxes { unsigned long long* box[kMaxG]; };   // box[g] on GPU g: [kMaxG] slots (one per sender)
+// box[g] on GPU g: [2][kMaxG] slots (step parity x sender).  Double buffering
+// by step parity: a sender can only reuse a parity slot (step s + 2) after it
+// received every peer's step s + 1, which each peer sends only after reading
+// the sender's step s -- no value is overwritten before it is read.
+struct Boxes { unsigned long long* box[kMaxG]; };
 
 __global__ void pingpong(Boxes B, int me, int G, int steps, unsigned long long* out) {
     if (threadIdx.x != 0) return;
@@ -29,7 +33,7 @@ __global__ void pingpong(Boxes B, int me, int G, int steps, unsigned long long* 
         const unsigned long long v = ((unsigned long long)s << 40) | (key & 0xFFFFFFFFFFull);
         for (int g = 0; g < G; ++g) {
             if (g == me) continue;
-            unsigned long long* dst = B.box[g] + me;
+            unsigned long long* dst = B.box[g] + (s & 1) * kMaxG + me;
             asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(v) : "memory");
         }
         unsigned long long mn = v;
@@ -37,7 +41,7 @@ __global__ void pingpong(Boxes B, int me, int G, int steps, unsigned long long* 
             if (g == me) continue;
             unsigned long long w;
             do {
-                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(B.box[me] + g) : "memory");
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(B.box[me] + (s & 1) * kMaxG + g) : "memory");
             } while ((w >> 40) != (unsigned long long)s);
             mn = w < mn ? w : mn;
         }
@@ -66,15 +70,15 @@ int main(int argc, char** argv) {
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
             cudaGetLastError();
         }
-        CK(cudaMalloc(&B.box[g], sizeof(unsigned long long) * kMaxG));
-        CK(cudaMemset(B.box[g], 0, sizeof(unsigned long long) * kMaxG));
+        CK(cudaMalloc(&B.box[g], sizeof(unsigned long long) * 2 * kMaxG));
+        CK(cudaMemset(B.box[g], 0, sizeof(unsigned long long) * 2 * kMaxG));
         CK(cudaMalloc(&outs[g], 8));
     }
     for (int g = 0; g < G; ++g) { CK(cudaSetDevice(g)); CK(cudaDeviceSynchronize()); }
     // warm-up run, then the timed one (all GPUs launched back to back)
     double best = 1e30;
     for (int rep = 0; rep < 3; ++rep) {
-        for (int g = 0; g < G; ++g) { CK(cudaSetDevice(g)); CK(cudaMemset(B.box[g], 0, sizeof(unsigned long long) * kMaxG)); CK(cudaDeviceSynchronize()); }
+        for (int g = 0; g < G; ++g) { CK(cudaSetDevice(g)); CK(cudaMemset(B.box[g], 0, sizeof(unsigned long long) * 2 * kMaxG)); CK(cudaDeviceSynchronize()); }
         const int n = rep == 0 ? 1000 : steps;
         auto t0 = std::chrono::steady_clock::now();
         for (int g = 0; g < G; ++g) { CK(cudaSetDevice(g)); pingpong<<<1, 32>>>(B, g, G, n, outs[g]); }
