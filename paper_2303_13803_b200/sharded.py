@@ -14,8 +14,8 @@ host-logic path the CPU/gloo tests exercise).
 Why the matching itself is not sharded (SURVEY.md §8e's K6): its critical
 path is a chain of dependent Dijkstra pops (~1.2 us each on one GPU, 8 SMs
 of a thread-block cluster).  Splitting the columns across GPUs adds an
-all-GPU minimum per pop: measured 3.2 us for a peer-memory exchange between
-2 GPUs and 21 us for an NCCL all-reduce of one int64
+all-GPU minimum per pop: measured 2.9 / 6.6 us for a peer-memory exchange among
+2 / 4 GPUs and 21 us for an NCCL all-reduce of one int64
 (profiles/r02/k6_*.json), i.e. every pop would get 3-18x slower.  The solve
 therefore stays on one GPU; `bench.py --gpus N` measures replicas (N
 snapshots, weak scaling) and reports this sharded round beside it.
