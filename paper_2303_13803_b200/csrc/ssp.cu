@@ -1163,7 +1163,10 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     const int32_t nloc = max(0, min(mc, m - c0));
     int64_t* psr = reinterpret_cast<int64_t*>(smem);                          // [m] prices (replicated)
     int32_t* rocr = reinterpret_cast<int32_t*>(psr + m);                      // [m] owners (replicated)
-    int32_t* pred = rocr + ((m + 1) & ~1);                                    // [mc] predecessor rows (local)
+    // CTA 0: colof[i] = the column whose pop brought row i into the tree (its
+    // matched column), so the augmenting-path walk stays in shared memory
+    int32_t* colof = rocr + ((m + 1) & ~1);                                  // [m] (CTA 0)
+    int32_t* pred = colof + ((m + 1) & ~1);                                  // [mc] predecessor rows (local)
     // two row-slice buffers for the runner-up prefetch (TMA bulk copies)
     const int32_t slot_words = ((mc + 8 + 3) & ~3);
     wt_t* rowbuf = reinterpret_cast<wt_t*>((reinterpret_cast<uintptr_t>(pred + mc) + 127) & ~(uintptr_t)127);
@@ -1243,6 +1246,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             const int32_t i = rocr[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (rank == 0 && tid == 0) colof[i] = jm;
             const long long tA = tm ? clock64() : 0;
             const wt_t* Ai = rowp(L, i);
             const int64_t aim = (int64_t)__ldg(Ai + jm);
@@ -1341,7 +1345,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                 while (true) {
                     const int owner = j / mc;
                     const int32_t ii = cluster.map_shared_rank(pred, owner)[j - owner * mc];
-                    const int32_t jn = (ii == s) ? -1 : __ldcg(L.cor + ii);
+                    const int32_t jn = (ii == s) ? -1 : colof[ii];
                     L.roc[j] = ii;
                     L.cor[ii] = j;
                     if (ii == s) break;
@@ -1605,7 +1609,8 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
     const int32_t m = L.m;
     int64_t* psr = reinterpret_cast<int64_t*>(smem);                          // [m] prices
     int32_t* rocr = reinterpret_cast<int32_t*>(psr + m);                      // [m] owners
-    int32_t* pred = rocr + ((m + 1) & ~1);                                    // [m] predecessor rows
+    int32_t* colof = rocr + ((m + 1) & ~1);                                  // [m] matched column of each tree row
+    int32_t* pred = colof + ((m + 1) & ~1);                                  // [m] predecessor rows
     const int tid = threadIdx.x, w = tid >> 5;
     int par = 0;
     unsigned long long steps = 0;
@@ -1668,6 +1673,7 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
             const int32_t i = rocr[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (tid == 0) colof[i] = jm;
             const long long tA = tm ? clock64() : 0;
             const wt_t* Ai = rowp(L, i);
             wt_t av[CC];
@@ -1712,7 +1718,7 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
                 int32_t j = jf;
                 while (true) {
                     const int32_t ii = pred[j];
-                    const int32_t jn = (ii == s) ? -1 : __ldcg(L.cor + ii);
+                    const int32_t jn = (ii == s) ? -1 : colof[ii];
                     L.roc[j] = ii;
                     L.cor[ii] = j;
                     if (ii == s) break;
@@ -2269,11 +2275,11 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
             // register-key kernel: 12 m replicated + 4 bytes per local column + two row-slice buffers
-            const size_t rk_bytes = 12ull * m + 8 + 4ull * mcl + 128 + 2ull * sizeof(wt_t) * ((mcl + 8 + 3) & ~3) + 64;
+            const size_t rk_bytes = 16ull * m + 16 + 4ull * mcl + 128 + 2ull * sizeof(wt_t) * ((mcl + 8 + 3) & ~3) + 64;
             const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8 && T.ssp_rslice != 2;
             const bool slice_ok = use_cluster && m <= CL * CTHREADS * CCOLS && cl_bytes <= xs_budget - 2048;
             // single SM for levels up to T.ssp_one columns: one barrier per pop, no DSMEM
-            const size_t r1_bytes = 16ull * m + 16;
+            const size_t r1_bytes = 20ull * m + 24;
             const bool rkey1_ok = m <= T.ssp_one && m <= 1024 * 10 && r1_bytes <= xs_budget - 2048;
             if (rkey1_ok) {
                 if (m <= 1024) ssp_rkey1_kernel<1><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
