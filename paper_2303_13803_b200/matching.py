@@ -3,11 +3,13 @@
 Mirrors /root/reference/pkg/src/muxsim/matching.py.  `max_weight_matching`
 keeps the reference's contract (sorted ids, zero padding to square, the 1e-6
 weight floor, only W > 0 pairs emitted, total summed in row order) but solves
-with the libmuxflow epsilon-scaling auction (csrc/auction.cu) on integer
-weights rint(w * 2^qbits).  Dyadic inputs with granularity >= 2^-qbits (all of
-the reference's tests) are solved exactly; general floats are solved exactly
-for their quantisation.  `match_dense` is the array-level entry the
-scheduling round and the benchmarks use.
+with libmuxflow's multilevel shortest-path solver (csrc/ssp.cu) on integer
+weights rint(w * 2^qbits), followed by the reference's tie canonicalisation
+(csrc/canon.cu).  Dyadic inputs with granularity >= 2^-qbits (all of the
+reference's tests) are solved exactly; general floats are solved exactly for
+their quantisation (an optimum of the quantised problem is within
+n * 2^-(qbits+1) of the float optimum).  `match_dense` / `match_dense_ptr`
+are the array-level entries the scheduling round and the benchmarks use.
 """
 
 import math
