@@ -2124,6 +2124,16 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<2, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<2, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<6, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<8, CL, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<4, CL, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<8, CL, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<12, CL, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<16, CL, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<1, CL, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<2, CL, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
@@ -2289,7 +2299,22 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
                 else if (m <= 8192) ssp_rkey1_kernel<8><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
                 else ssp_rkey1_kernel<10><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
             } else if (rkey_ok) {
-                if (mcl <= 512) ssp_rkey_kernel<1, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                // 256 threads per CTA (default): fewer warps per barrier, 1.16 -> 1.08 us/pop at 10k
+                // against 512; 128 / 512 / 1024 stay selectable (MUX_SSP_CT) for A/B runs
+                if (T.ssp_ct == 256) {
+                    if (mcl <= 512) ssp_rkey_kernel<2, CL, 256><<<CL, 256, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else if (mcl <= 1024) ssp_rkey_kernel<4, CL, 256><<<CL, 256, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else if (mcl <= 1536) ssp_rkey_kernel<6, CL, 256><<<CL, 256, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else ssp_rkey_kernel<8, CL, 256><<<CL, 256, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                } else if (T.ssp_ct == 128) {
+                    if (mcl <= 512) ssp_rkey_kernel<4, CL, 128><<<CL, 128, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else if (mcl <= 1024) ssp_rkey_kernel<8, CL, 128><<<CL, 128, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else if (mcl <= 1536) ssp_rkey_kernel<12, CL, 128><<<CL, 128, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else ssp_rkey_kernel<16, CL, 128><<<CL, 128, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                } else if (T.ssp_ct == 1024) {
+                    if (mcl <= 1024) ssp_rkey_kernel<1, CL, 1024><<<CL, 1024, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                    else ssp_rkey_kernel<2, CL, 1024><<<CL, 1024, rk_bytes, st>>>(L, ndef_total, pl, cpush);
+                } else if (mcl <= 512) ssp_rkey_kernel<1, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 1024) ssp_rkey_kernel<2, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 1536) ssp_rkey_kernel<3, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);
                 else ssp_rkey_kernel<4, CL, 512><<<CL, 512, rk_bytes, st>>>(L, ndef_total, pl, cpush);

@@ -140,11 +140,14 @@ def test_long_path_kernels_agree(cuda, certified, tuning, monkeypatch):
         assert total == want, env
 
 
-@pytest.mark.parametrize("env", [{"MUX_SSP_PF": "0"}, {"MUX_SSP_PF": "1"}])
+@pytest.mark.parametrize("env", [{"MUX_SSP_PF": "0"}, {"MUX_SSP_PF": "1"}] +
+                         [{"MUX_SSP_CT": ct} for ct in ("128", "256", "512", "1024")])
 def test_long_path_prefetch_variants(cuda, certified, tuning, monkeypatch, env):
-    """The long-path kernel (csrc/ssp.cu ssp_rkey_kernel) with and without the
-    runner-up row prefetch gives the same optimum; the dual certificate is
-    checked at every level (MUX_SSP_CHECK=1)."""
+    """The long-path kernel (csrc/ssp.cu ssp_rkey_kernel; MUX_SSP_ONE=0 keeps
+    every level off the single-SM kernel) with and without the runner-up row
+    prefetch and at every CTA size gives the same optimum; the dual
+    certificate is checked at every level (MUX_SSP_CHECK=1)."""
+    monkeypatch.setenv("MUX_SSP_ONE", "0")
     cl, Q = _pred_Q(2000, 32, 30)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -268,6 +271,10 @@ def test_tuning_knobs_are_gated_and_validated(cuda, monkeypatch):
         _match(Q)
     monkeypatch.delenv("MUX_SOLVER")
     with pytest.raises(nat.NativeError, match="MUX_SSP_F=99"):
+        _match(Q)
+    monkeypatch.delenv("MUX_SSP_F")
+    monkeypatch.setenv("MUX_SSP_CT", "384")      # in range, not a compiled CTA size
+    with pytest.raises(nat.NativeError, match="MUX_SSP_CT must be"):
         _match(Q)
 
 
