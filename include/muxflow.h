@@ -84,7 +84,7 @@ typedef struct {
     int64_t n_cols;          /* M (real offline columns)                  */
     int64_t n_square;        /* max(N, M): the padded square size          */
     int64_t phases;          /* epsilon-scaling phases run                 */
-    int64_t rounds;          /* parallel bidding rounds (grid barriers)    */
+    int64_t rounds;          /* auction: bidding rounds (grid barriers); ssp: long-path exchange steps */
     int64_t bids;            /* accepted + rejected bids                   */
     int64_t row_scans;       /* full weight-row reads                      */
     int64_t tail_bids;       /* bids made in single-CTA tail mode          */

@@ -58,13 +58,16 @@ const Tuning& tuning() {
         t.ssp_deep = knob("MUX_SSP_DEEP", t.ssp_deep, 0, 1000, err);
         t.ssp_coarse_pops = knob("MUX_SSP_COARSE_POPS", 0, 0, 1000000000, err);
         t.ssp_serial = knob("MUX_SSP_SERIAL", 0, 0, 1, err) == 1;
-        t.ssp_pf = knob("MUX_SSP_PF", 1, 0, 1, err) == 1;
+        t.ssp_pf = knob("MUX_SSP_PF", t.ssp_pf ? 1 : 0, 0, 1, err) == 1;
+        t.ssp_l2pf = knob("MUX_SSP_L2PF", t.ssp_l2pf ? 1 : 0, 0, 1, err) == 1;
+        t.ssp_ties = knob("MUX_SSP_TIES", t.ssp_ties ? 1 : 0, 0, 1, err) == 1;
         t.ssp_cluster = knob("MUX_SSP_CLUSTER", 1, 0, 1, err) == 1;
         t.ssp_sparsex = knob("MUX_SSP_SPARSEX", 0, 0, 1, err) == 1;
         t.ssp_one = knob("MUX_SSP_ONE", t.ssp_one, 0, 10240, err);
         t.ssp_ct = knob("MUX_SSP_CT", t.ssp_ct, 128, 1024, err);
         if (t.ssp_ct != 128 && t.ssp_ct != 256 && t.ssp_ct != 512 && t.ssp_ct != 1024 && err.empty()) err = "MUX_SSP_CT must be 128, 256, 512 or 1024";
         t.ssp_rslice = knob("MUX_SSP_RSLICE", 1, 0, 2, err);
+        t.ssp_dump = getenv("MUX_SSP_DUMP");
         t.auc_theta = knob("MUX_THETA", t.auc_theta, 2, 64, err);
         t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 1 << 20, err);   // clamped to the tail buffer inside
         t.auc_k = knob("MUX_K", t.auc_k, 1, 15, err);

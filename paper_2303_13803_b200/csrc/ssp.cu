@@ -99,6 +99,8 @@ struct Cnt {
     long long xcyc[4];   // exclusive kernel: pop, horizon re-scans, scan steps, augment
     unsigned long long xpfhits;   // register-key kernel: pops whose row slice was prefetched into smem
     unsigned long long xwalk, xwalkcyc, xsearch, xsynccyc;   // timing mode: augmenting-path walk steps / cycles, searches
+    unsigned long long xrounds;   // register-key kernel: exchange steps (pops minus batched ties)
+    unsigned long long xt[5];     // timing mode: load+relax cycles / steps of prefetch-hit steps, of tie steps; push-to-arrival cycles
 };
 
 struct Lvl {
@@ -1011,6 +1013,96 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
     return r;
 }
 
+// Tie batching (the register-key kernel): warp minima at the winner's
+// distance are popped in the same step -- Dijkstra may settle columns of equal
+// distance in any order, and a relaxation from one of them cannot take another
+// below that distance.  Only matched winners batch (a free winner ends the
+// search; free columns sort first, so none ties with a matched winner).
+constexpr int kTieMax = 3;
+struct CTies {
+    uint64_t key[2][kTieMax];
+    int32_t n[2];
+};
+
+// cluster_min_push that also returns up to kTieMax further warp minima at the
+// winner's distance (tk[0..nt)); cand2 skips every key at that distance.
+template <int CLS, int NW>
+__device__ __forceinline__ uint64_t cluster_min_push_ties(uint64_t v, CShared& S, CPush<CLS>& P, CTies& T, int& par,
+                                                          uint32_t& ph, int rank, uint64_t& cand2, uint64_t (&tk)[kTieMax],
+                                                          int& nt, bool ties, unsigned long long* tw = nullptr) {
+    const long long tw0 = tw ? clock64() : 0;
+    v = wmin64(v);
+    const int w = threadIdx.x >> 5, ln = lane_id();
+    const uint32_t lb = smem_u32(&P.bar[par]);
+    if (ln < CLS) {
+        const uint32_t la = smem_u32(&P.slots[par][rank * 32 + w]);
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(ln));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(ln));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(ra), "l"(v), "r"(rb)
+                     : "memory");
+    }
+    if (w == 0) {
+        const uint32_t parity = (ph >> par) & 1u;
+        uint32_t done = 0;
+        while (!done) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(lb), "r"(parity)
+                : "memory");
+        }
+        if (tw) *tw += clock64() - tw0;
+        // the CLS x NW warp minima spread over all 32 lanes (KPL each): short
+        // dependency chains for the minimum and the tie list
+        constexpr int TOT = CLS * NW, KPL = (TOT + 31) / 32;
+        uint64_t ys[KPL];
+        uint64_t x = kNoKey;
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const int e = ln + 32 * k;
+            ys[k] = e < TOT ? P.slots[par][(e / NW) * 32 + (e % NW)] : kNoKey;
+            x = ys[k] < x ? ys[k] : x;
+        }
+        x = wmin64(x);
+        const uint64_t dhi = x >> kSH;
+        const bool batch = ties && (x & kFreeBit) != 0 && x != kNoKey;
+        const unsigned lt = (1u << ln) - 1u;
+        uint64_t c2 = kNoKey;
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const uint64_t y = ys[k];
+            const bool same = (y >> kSH) == dhi;
+            const bool tie = batch && same && y != x;
+            const unsigned msk = __ballot_sync(~0u, tie);
+            if (tie) {
+                const int pos = cnt + __popc(msk & lt);
+                if (pos < kTieMax) T.key[par][pos] = y;
+            }
+            cnt += __popc(msk);
+            if (ties ? !same : y != x) c2 = y < c2 ? y : c2;
+        }
+        cand2 = c2;
+        if (ln == 0) {
+            S.bkey[par] = x;
+            T.n[par] = cnt < kTieMax ? cnt : kTieMax;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 8) : "memory");
+        }
+    }
+    ph ^= 1u << par;
+    __syncthreads();
+    const uint64_t r = S.bkey[par];
+    nt = ties ? T.n[par] : 0;
+    uint64_t raw[kTieMax];
+#pragma unroll
+    for (int t = 0; t < kTieMax; ++t) raw[t] = T.key[par][t];   // independent of nt: loads in parallel
+#pragma unroll
+    for (int t = 0; t < kTieMax; ++t) tk[t] = t < nt ? raw[t] : kNoKey;
+    par ^= 1;
+    return r;
+}
+
 // Sliced long-path kernel (m too large to replicate prices and owners in
 // every CTA: the 10k x 40k rounds).  Per local column: distance, price,
 // predecessor, owner, scanned flag in shared memory (25 bytes).
@@ -1155,6 +1247,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CShared S;
     __shared__ __align__(16) CPush<CLS> P;
+    __shared__ CTies TS;
     cg::cluster_group cluster = cg::this_cluster();
     const int32_t m = L.m;
     const int32_t mc = (m + CLS - 1) / CLS;
@@ -1174,15 +1267,20 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     __shared__ int32_t pfrow[2], pfshift[2];
     __shared__ uint32_t pfpar[2];
     const bool pf = (push & 4) != 0;
+    const bool l2pf = (push & 32) != 0;
+    const bool ties = (push & 64) != 0;
     uint32_t pfcount[2] = {0, 0};   // tid 0: copies issued per slot
     int cur = 0;
     const int tid = threadIdx.x;
     int par = 0;
     uint32_t ph = 0;
     uint64_t cand2 = kNoKey;
-    unsigned long long steps = 0, pfhits = 0;
+    unsigned long long steps = 0, pfhits = 0, rounds = 0;
+    uint64_t tk[kTieMax];
+    int nt = 0;
     const bool tm = (push & 16) != 0;
     long long tcyc[3] = {0, 0, 0};
+    unsigned long long txt[5] = {0, 0, 0, 0, 0};
     if (tid < 64) S.slots[tid >> 5][tid & 31] = kNoKey;
     if (tid < 2) {
         pfrow[tid] = -1;
@@ -1228,7 +1326,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                 pk[u] = kTop;
             }
         }
-        const uint64_t k0 = cluster_min_push<CLS, NT / 32>(vmin, S, P, par, ph, rank, cand2);
+        const uint64_t k0 = cluster_min_push_ties<CLS, NT / 32>(vmin, S, P, TS, par, ph, rank, cand2, tk, nt, ties);
         const int64_t pis = -((int64_t)(k0 >> kSH) - kDistLim);
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
@@ -1236,6 +1334,8 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             kd[u] = jj < nloc ? (((uint64_t)pis << kSH) + pk[u] - ((uint64_t)as[u] << kSH)) : kNoKey;
         }
         uint64_t best = k0 & kLowMask;   // distance 0, same column and free bit
+#pragma unroll
+        for (int t = 0; t < kTieMax; ++t) tk[t] &= kLowMask;   // ties at distance 0
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
@@ -1245,31 +1345,44 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             const int64_t dmin = (int64_t)(best >> kSH);
             const int32_t i = rocr[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
-            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (rank == 0 && tid == 0) colof[i] = jm;
+            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (rank == 0 && tid == 0) {
+                colof[i] = jm;
+#pragma unroll
+                for (int t = 0; t < kTieMax; ++t)
+                    if (t < nt) colof[rocr[tk[t] & kIdxMask]] = (int32_t)(tk[t] & kIdxMask);
+            }
             const long long tA = tm ? clock64() : 0;
             const wt_t* Ai = rowp(L, i);
             const int64_t aim = (int64_t)__ldg(Ai + jm);
             wt_t av[CC];
-            if (pf && pfrow[cur] == i) {
-                // the runner-up of the previous step: its slice is (being) copied into smem
-                const uint32_t bar = smem_u32(&pfbar[cur]), parity = pfpar[cur];
-                uint32_t done = 0;
-                while (!done)
-                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-                const wt_t* rb = rowbuf + cur * slot_words + pfshift[cur];
-#pragma unroll
-                for (int u = 0; u < CC; ++u) {
-                    const int32_t jj = tid + u * NT;
-                    av[u] = jj < nloc ? rb[jj] : 0;
-                }
-                ++pfhits;
-            } else {
+            // the runner-up of the previous step has its slice (being) copied into smem;
+            // its barrier is waited on only after every global load of this step is issued
+            const bool hit = pf && pfrow[cur] == i;
+            if (!hit) {
 #pragma unroll
                 for (int u = 0; u < CC; ++u) {
                     const int32_t jj = tid + u * NT;
                     av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
+                }
+            }
+            // the tied columns' rows (matched: a tie never carries the free flag); their
+            // bases are formed at the relaxation so no load result is waited on here
+            wt_t avt[kTieMax][CC];
+            wt_t aimt[kTieMax];
+            int32_t it[kTieMax];
+#pragma unroll
+            for (int t = 0; t < kTieMax; ++t) {
+                if (t < nt) {
+                    const int32_t jt = (int32_t)(tk[t] & kIdxMask);
+                    it[t] = rocr[jt];
+                    const wt_t* At = rowp(L, it[t]);
+                    aimt[t] = __ldg(At + jt);
+#pragma unroll
+                    for (int u = 0; u < CC; ++u) {
+                        const int32_t jj = tid + u * NT;
+                        avt[t][u] = jj < nloc ? __ldg(At + c0 + jj) : 0;
+                    }
                 }
             }
             // runner-up prefetch: warp 0 copies this CTA's slice of the row owning the
@@ -1304,11 +1417,46 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                     }
                 }
             }
-            // pop jm: its owner thread marks it scanned
+            // L2 prefetch: every lane's candidate (its warp-index minimum other than the
+            // winner, one of the next few pops) gets this CTA's slice of its row pulled
+            // from HBM into L2
+            if (l2pf && tid < NT / 32 && cand2 != kNoKey && nloc > 0) {
+                const int32_t i2 = rocr[cand2 & kIdxMask];
+                if (i2 >= 0) {
+                    const wt_t* src = rowp(L, i2) + c0;
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+                }
+            }
+            // pop jm and the ties: their owner threads mark them scanned
             if (jm >= c0 && jm < c0 + nloc) {
 #pragma unroll
                 for (int u = 0; u < CC; ++u)
                     if (jm - c0 == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+            }
+#pragma unroll
+            for (int t = 0; t < kTieMax; ++t) {
+                const int32_t jt = (int32_t)(tk[t] & kIdxMask) - c0;   // tk = kNoKey past nt: out of range
+                if (t < nt && jt >= 0 && jt < nloc) {
+#pragma unroll
+                    for (int u = 0; u < CC; ++u)
+                        if (jt == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+                }
+            }
+            if (hit) {
+                const uint32_t bar = smem_u32(&pfbar[cur]), parity = pfpar[cur];
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+                const wt_t* rb = rowbuf + cur * slot_words + pfshift[cur];
+#pragma unroll
+                for (int u = 0; u < CC; ++u) {
+                    const int32_t jj = tid + u * NT;
+                    av[u] = jj < nloc ? rb[jj] : 0;
+                }
+                ++pfhits;
             }
             const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << kSH;
             best = kNoKey;
@@ -1316,15 +1464,33 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             for (int u = 0; u < CC; ++u) {
                 const uint64_t nk = base + pk[u] - ((uint64_t)av[u] << kSH);
                 if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
-                best = kd[u] < best ? kd[u] : best;
             }
+#pragma unroll
+            for (int t = 0; t < kTieMax; ++t) {
+                if (t < nt) {
+                    const int32_t jt = (int32_t)(tk[t] & kIdxMask);
+                    const uint64_t b = (uint64_t)(dmin + (int64_t)aimt[t] - psr[jt]) << kSH;
+#pragma unroll
+                    for (int u = 0; u < CC; ++u) {
+                        const uint64_t nk = b + pk[u] - ((uint64_t)avt[t][u] << kSH);
+                        if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = it[t]; }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < CC; ++u) best = kd[u] < best ? kd[u] : best;
+            steps += nt;
+            ++rounds;
+            const int nt_step = nt;
             const long long tB = tm ? clock64() : 0;
-            best = cluster_min_push<CLS, NT / 32>(best, S, P, par, ph, rank, cand2);
+            best = cluster_min_push_ties<CLS, NT / 32>(best, S, P, TS, par, ph, rank, cand2, tk, nt, ties, tm && tid == 0 ? &txt[4] : nullptr);
             if (tm) {
                 const long long tC = clock64();
                 tcyc[0] += tB - tA;
                 tcyc[1] += tC - tB;
                 tcyc[2] += 1;
+                if (hit) { txt[0] += tB - tA; txt[1] += 1; }
+                if (nt_step > 0) { txt[2] += tB - tA; txt[3] += 1; }
             }
             cur ^= 1;
             ++steps;
@@ -1369,9 +1535,12 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     if (rank == 0 && tid == 0) {
         atomicAdd(&L.cnt->xsteps, steps);
         atomicAdd(&L.cnt->xpfhits, pfhits);
+        atomicAdd(&L.cnt->xrounds, rounds);
     }
     if (tm && rank == 0 && tid == 0)
         for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
+    if (tm && rank == 0 && tid == 0)
+        for (int k = 0; k < 5; ++k) atomicAdd(&L.cnt->xt[k], txt[k]);
 }
 
 // Register-key kernel for levels too large to replicate prices and owners
@@ -2147,7 +2316,7 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     // register-key kernel flags: 4 = runner-up row prefetch into shared memory, 16 = per-pop cycle timing
-    const int32_t cpush = (T.ssp_pf ? 4 : 0) | (T.ssp_time ? 16 : 0);
+    const int32_t cpush = (T.ssp_pf ? 4 : 0) | (T.ssp_time ? 16 : 0) | (T.ssp_l2pf ? 32 : 0) | (T.ssp_ties ? 64 : 0);
     const bool use_cluster = T.ssp_cluster;
     int per_sm = 0;
     MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ssp_parallel_kernel, PWARPS * 32, psmem));
@@ -2284,6 +2453,31 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
             const int32_t mcl = (m + CL - 1) / CL;
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
+            if (T.ssp_dump) {
+                // analysis dump: header {m, nreal, ndef, level}, A rows [nreal][m], p, roc, cor, defer
+                static int seq = 0;
+                MUX_CUDA_TRY(cudaStreamSynchronize(st));
+                std::vector<wt_t> a((size_t)L.nreal * m);
+                MUX_CUDA_TRY(cudaMemcpy2D(a.data(), sizeof(wt_t) * m, L.A, sizeof(wt_t) * L.lda, sizeof(wt_t) * m, L.nreal,
+                                          cudaMemcpyDeviceToHost));
+                std::vector<int64_t> hp(m);
+                std::vector<int32_t> hroc(m), hcor(m), hdef(ndef_total);
+                MUX_CUDA_TRY(cudaMemcpy(hp.data(), L.p, 8ull * m, cudaMemcpyDeviceToHost));
+                MUX_CUDA_TRY(cudaMemcpy(hroc.data(), L.roc, 4ull * m, cudaMemcpyDeviceToHost));
+                MUX_CUDA_TRY(cudaMemcpy(hcor.data(), L.cor, 4ull * m, cudaMemcpyDeviceToHost));
+                MUX_CUDA_TRY(cudaMemcpy(hdef.data(), L.defer, 4ull * ndef_total, cudaMemcpyDeviceToHost));
+                const std::string path = std::string(T.ssp_dump) + "/lvl" + std::to_string(l) + "_" + std::to_string(seq++) + ".bin";
+                if (FILE* f = fopen(path.c_str(), "wb")) {
+                    const int32_t hdr[5] = {m, L.nreal, ndef_total, l, (int32_t)sizeof(wt_t)};
+                    fwrite(hdr, 4, 5, f);
+                    fwrite(a.data(), sizeof(wt_t), a.size(), f);
+                    fwrite(hp.data(), 8, m, f);
+                    fwrite(hroc.data(), 4, m, f);
+                    fwrite(hcor.data(), 4, m, f);
+                    fwrite(hdef.data(), 4, ndef_total, f);
+                    fclose(f);
+                }
+            }
             // register-key kernel: 12 m replicated + 4 bytes per local column + two row-slice buffers
             const size_t rk_bytes = 16ull * m + 16 + 4ull * mcl + 128 + 2ull * sizeof(wt_t) * ((mcl + 8 + 3) & ~3) + 64;
             const bool rkey_ok = use_cluster && mcl <= 512 * 4 && rk_bytes <= xs_budget - 2048 - push_b8 && T.ssp_rslice != 2;
@@ -2433,7 +2627,7 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     if (stats) {
         stats->n_rows = N; stats->n_cols = M; stats->n_square = n;
         stats->phases = nl;
-        stats->rounds = 0;
+        stats->rounds = (int64_t)hc.xrounds;
         stats->bids = (int64_t)(hc.steps + hc.xsteps);
         stats->row_scans = (int64_t)(hc.deep + hc.xdeep + hc.refresh);
         stats->tail_bids = (int64_t)hc.xsteps;
@@ -2459,6 +2653,10 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
                 (long long)hc.xcyc[2], hc.xcyc[0] / k, hc.xcyc[1] / k, (double)hc.xpfhits / (double)std::max(1ull, hc.xsteps),
                 hc.xsearch, hc.xwalk, (double)hc.xwalkcyc / (double)std::max(1ull, hc.xwalk),
                 (double)hc.xsynccyc / (double)std::max(1ull, hc.xsearch));
+        fprintf(stderr, "[ssp-time] register-key steps %llu: push-to-arrival %.0f cycles | prefetch-hit %llu (load+relax %.0f cycles), "
+                        "tie steps %llu (load+relax %.0f)\n",
+                hc.xrounds, (double)hc.xt[4] / (double)std::max(1ull, hc.xrounds), hc.xt[1],
+                (double)hc.xt[0] / (double)std::max(1ull, hc.xt[1]), hc.xt[3], (double)hc.xt[2] / (double)std::max(1ull, hc.xt[3]));
     }
     return MUX_OK;
 }

@@ -140,13 +140,15 @@ def test_long_path_kernels_agree(cuda, certified, tuning, monkeypatch):
         assert total == want, env
 
 
-@pytest.mark.parametrize("env", [{"MUX_SSP_PF": "0"}, {"MUX_SSP_PF": "1"}] +
+@pytest.mark.parametrize("env", [{"MUX_SSP_PF": "0"}, {"MUX_SSP_PF": "1"}, {"MUX_SSP_TIES": "0"},
+                                 {"MUX_SSP_TIES": "0", "MUX_SSP_PF": "1"}, {"MUX_SSP_L2PF": "1"}] +
                          [{"MUX_SSP_CT": ct} for ct in ("128", "256", "512", "1024")])
 def test_long_path_prefetch_variants(cuda, certified, tuning, monkeypatch, env):
     """The long-path kernel (csrc/ssp.cu ssp_rkey_kernel; MUX_SSP_ONE=0 keeps
-    every level off the single-SM kernel) with and without the runner-up row
-    prefetch and at every CTA size gives the same optimum; the dual
-    certificate is checked at every level (MUX_SSP_CHECK=1)."""
+    every level off the single-SM kernel) with and without tie batching, the
+    runner-up row prefetch and the L2 prefetch, and at every CTA size, gives
+    the same optimum; the dual certificate is checked at every level
+    (MUX_SSP_CHECK=1)."""
     monkeypatch.setenv("MUX_SSP_ONE", "0")
     cl, Q = _pred_Q(2000, 32, 30)
     for k, v in env.items():

@@ -27,5 +27,6 @@ for r in range(reps):
     ms = (time.perf_counter() - t0) * 1e3
     d = st.as_dict()
     print(f"round {r}: {ms:.2f} ms total {tot.value} dense {d['ms_dense']:.2f} ms pops {d['dense_steps']} "
-          f"us/pop {1e3 * d['ms_dense'] / max(1, d['dense_steps']):.3f} parallel {d['ms_parallel']:.2f} canon {d['ms_canon']:.2f}",
+          f"us/pop {1e3 * d['ms_dense'] / max(1, d['dense_steps']):.3f} steps {d['rounds']} "
+          f"us/step {1e3 * d['ms_dense'] / max(1, d['rounds']):.3f} parallel {d['ms_parallel']:.2f} canon {d['ms_canon']:.2f}",
           flush=True)
