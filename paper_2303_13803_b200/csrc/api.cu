@@ -67,6 +67,8 @@ const Tuning& tuning() {
         t.ssp_ct = knob("MUX_SSP_CT", t.ssp_ct, 128, 1024, err);
         if (t.ssp_ct != 128 && t.ssp_ct != 256 && t.ssp_ct != 512 && t.ssp_ct != 1024 && err.empty()) err = "MUX_SSP_CT must be 128, 256, 512 or 1024";
         t.ssp_rslice = knob("MUX_SSP_RSLICE", 1, 0, 2, err);
+        t.ssp_ct1 = knob("MUX_SSP_CT1", t.ssp_ct1, 512, 1024, err);
+        if (t.ssp_ct1 != 512 && t.ssp_ct1 != 1024 && err.empty()) err = "MUX_SSP_CT1 must be 512 or 1024";
         t.ssp_dump = getenv("MUX_SSP_DUMP");
         t.auc_theta = knob("MUX_THETA", t.auc_theta, 2, 64, err);
         t.auc_tail = knob("MUX_TAIL", t.auc_tail, -1, 1 << 20, err);   // clamped to the tail buffer inside

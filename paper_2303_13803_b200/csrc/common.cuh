@@ -67,6 +67,7 @@ struct Tuning {
     bool ssp_cluster = true;     // MUX_SSP_CLUSTER=0: single-CTA / single-warp long paths
     bool ssp_sparsex = false;    // MUX_SSP_SPARSEX=1: single-warp sparse long paths
     int ssp_rslice = 1;          // MUX_SSP_RSLICE [0, 2]: 0 = large levels on the shared-memory sliced kernel, 2 = every cluster level on it
+    int ssp_ct1 = 512;           // MUX_SSP_CT1 {512, 1024}: threads of the single-SM long-path kernel (levels <= 3072)
     int ssp_ct = 256;            // MUX_SSP_CT {128, 256, 512, 1024}: threads per CTA of the long-path kernel
     const char* ssp_dump = nullptr;   // MUX_SSP_DUMP=dir: write each long-search batch's level state (analysis)
     int ssp_one = 2560;          // MUX_SSP_ONE [0, 10240]: levels up to this size run long paths on one SM

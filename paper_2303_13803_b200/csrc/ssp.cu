@@ -1770,11 +1770,10 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
 // one SM, and a block-wide minimum with ONE barrier per pop -- every warp
 // writes its minimum to a parity-double-buffered slot array, and after the
 // barrier every warp reduces the 32 slots itself.  No DSMEM round trip.
-template <int CC>
-__global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
-    constexpr int NT = 1024;
+template <int CC, int NT>
+__global__ void __launch_bounds__(NT, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint64_t slots[2][32];
+    __shared__ uint64_t slots[2][32];   // per-warp minima (slots past NT / 32 stay kNoKey)
     const int32_t m = L.m;
     int64_t* psr = reinterpret_cast<int64_t*>(smem);                          // [m] prices
     int32_t* rocr = reinterpret_cast<int32_t*>(psr + m);                      // [m] owners
@@ -1784,15 +1783,34 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
     int par = 0;
     unsigned long long steps = 0;
     const bool tm = (flags & 16) != 0;
+    const bool ties = (flags & 64) != 0;
     long long tcyc[3] = {0, 0, 0};
+    unsigned long long rounds = 0;
+    uint64_t tk[kTieMax];
+    int nt = 0;
+    // block minimum; with tie batching, also up to kTieMax further warp minima
+    // at the winner's distance (every warp derives the same list from the slots)
     auto block_min = [&](uint64_t v) -> uint64_t {
         v = wmin64(v);
         if (lane_id() == 0) slots[par][w] = v;
         __syncthreads();
-        const uint64_t x = wmin64(slots[par][lane_id()]);
+        const uint64_t y = slots[par][lane_id()];
+        const uint64_t x = wmin64(y);
+        const bool batch = ties && (x & kFreeBit) != 0 && x != kNoKey;
+        unsigned msk = __ballot_sync(~0u, batch && (y >> kSH) == (x >> kSH) && y != x);
+        nt = min(__popc(msk), kTieMax);
+#pragma unroll
+        for (int t = 0; t < kTieMax; ++t) {
+            const int l = __ffs(msk) - 1;
+            const uint64_t yt = __shfl_sync(~0u, y, l < 0 ? 0 : l);
+            tk[t] = t < nt ? yt : kNoKey;
+            msk &= msk - 1;
+        }
         par ^= 1;
         return x;
     };
+    if (tid < 64) slots[tid >> 5][tid & 31] = kNoKey;
+    __syncthreads();
     for (int32_t q = 0; q < ndef; ++q) {
         const int32_t s = L.defer[q];
         const wt_t* As = rowp(L, s);
@@ -1832,6 +1850,8 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
             kd[u] = j < m ? (((uint64_t)pis << kSH) + pk[u] - ((uint64_t)as[u] << kSH)) : kNoKey;
         }
         uint64_t best = k0 & kLowMask;
+#pragma unroll
+        for (int t = 0; t < kTieMax; ++t) tk[t] &= kLowMask;   // ties at distance 0
         int32_t jf;
         int64_t D;
         int32_t pops = 0;
@@ -1841,8 +1861,13 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
             const int64_t dmin = (int64_t)(best >> kSH);
             const int32_t i = rocr[jm];
             if (i < 0) { jf = jm; D = dmin; break; }
-            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (tid == 0) colof[i] = jm;
+            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (tid == 0) {
+                colof[i] = jm;
+#pragma unroll
+                for (int t = 0; t < kTieMax; ++t)
+                    if (t < nt) colof[rocr[tk[t] & kIdxMask]] = (int32_t)(tk[t] & kIdxMask);
+            }
             const long long tA = tm ? clock64() : 0;
             const wt_t* Ai = rowp(L, i);
             wt_t av[CC];
@@ -1852,17 +1877,58 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
                 av[u] = j < m ? __ldg(Ai + j) : 0;
             }
             const int64_t aim = (int64_t)__ldg(Ai + jm);
+            wt_t avt[kTieMax][CC];
+            wt_t aimt[kTieMax];
+            int32_t it[kTieMax];
+#pragma unroll
+            for (int t = 0; t < kTieMax; ++t) {
+                if (t < nt) {
+                    const int32_t jt = (int32_t)(tk[t] & kIdxMask);
+                    it[t] = rocr[jt];
+                    const wt_t* At = rowp(L, it[t]);
+                    aimt[t] = __ldg(At + jt);
+#pragma unroll
+                    for (int u = 0; u < CC; ++u) {
+                        const int32_t j = tid + u * NT;
+                        avt[t][u] = j < m ? __ldg(At + j) : 0;
+                    }
+                }
+            }
 #pragma unroll
             for (int u = 0; u < CC; ++u)
                 if (jm == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+#pragma unroll
+            for (int t = 0; t < kTieMax; ++t) {
+                const int32_t jt = (int32_t)(tk[t] & kIdxMask);
+                if (t < nt) {
+#pragma unroll
+                    for (int u = 0; u < CC; ++u)
+                        if (jt == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+                }
+            }
             const uint64_t base = (uint64_t)(dmin + aim - psr[jm]) << kSH;
             best = kNoKey;
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
                 const uint64_t nk = base + pk[u] - ((uint64_t)av[u] << kSH);
                 if (tid + u * NT < m && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
-                best = kd[u] < best ? kd[u] : best;
             }
+#pragma unroll
+            for (int t = 0; t < kTieMax; ++t) {
+                if (t < nt) {
+                    const int32_t jt = (int32_t)(tk[t] & kIdxMask);
+                    const uint64_t b = (uint64_t)(dmin + (int64_t)aimt[t] - psr[jt]) << kSH;
+#pragma unroll
+                    for (int u = 0; u < CC; ++u) {
+                        const uint64_t nk = b + pk[u] - ((uint64_t)avt[t][u] << kSH);
+                        if (tid + u * NT < m && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = it[t]; }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < CC; ++u) best = kd[u] < best ? kd[u] : best;
+            steps += nt;
+            ++rounds;
             const long long tB = tm ? clock64() : 0;
             best = block_min(best);
             if (tm) {
@@ -1898,7 +1964,10 @@ __global__ void __launch_bounds__(1024, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef,
         __threadfence();
         __syncthreads();
     }
-    if (tid == 0) atomicAdd(&L.cnt->xsteps, steps);
+    if (tid == 0) {
+        atomicAdd(&L.cnt->xsteps, steps);
+        atomicAdd(&L.cnt->xrounds, rounds);
+    }
     if (tm && tid == 0)
         for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
 }
@@ -2308,12 +2377,17 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<16, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<1, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<2, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<3, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<6, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<1, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<2, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<3, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<5, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<10, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     // register-key kernel flags: 4 = runner-up row prefetch into shared memory, 16 = per-pop cycle timing
     const int32_t cpush = (T.ssp_pf ? 4 : 0) | (T.ssp_time ? 16 : 0) | (T.ssp_l2pf ? 32 : 0) | (T.ssp_ties ? 64 : 0);
@@ -2486,12 +2560,18 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
             const size_t r1_bytes = 20ull * m + 24;
             const bool rkey1_ok = m <= T.ssp_one && m <= 1024 * 10 && r1_bytes <= xs_budget - 2048;
             if (rkey1_ok) {
-                if (m <= 1024) ssp_rkey1_kernel<1><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
-                else if (m <= 2048) ssp_rkey1_kernel<2><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
-                else if (m <= 3072) ssp_rkey1_kernel<3><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
-                else if (m <= 5120) ssp_rkey1_kernel<5><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
-                else if (m <= 8192) ssp_rkey1_kernel<8><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
-                else ssp_rkey1_kernel<10><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                // 512 threads (128 registers: the tie rows stay in registers) up to 3072 columns
+                if (T.ssp_ct1 == 512 && m <= 512) ssp_rkey1_kernel<1, 512><<<1, 512, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (T.ssp_ct1 == 512 && m <= 1024) ssp_rkey1_kernel<2, 512><<<1, 512, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (T.ssp_ct1 == 512 && m <= 1536) ssp_rkey1_kernel<3, 512><<<1, 512, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (T.ssp_ct1 == 512 && m <= 2048) ssp_rkey1_kernel<4, 512><<<1, 512, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (T.ssp_ct1 == 512 && m <= 3072) ssp_rkey1_kernel<6, 512><<<1, 512, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 1024) ssp_rkey1_kernel<1, 1024><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 2048) ssp_rkey1_kernel<2, 1024><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 3072) ssp_rkey1_kernel<3, 1024><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 5120) ssp_rkey1_kernel<5, 1024><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else if (m <= 8192) ssp_rkey1_kernel<8, 1024><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
+                else ssp_rkey1_kernel<10, 1024><<<1, 1024, r1_bytes, st>>>(L, ndef_total, pl, cpush);
             } else if (rkey_ok) {
                 // 256 threads per CTA (default): fewer warps per barrier, 1.16 -> 1.08 us/pop at 10k
                 // against 512; 128 / 512 / 1024 stay selectable (MUX_SSP_CT) for A/B runs
