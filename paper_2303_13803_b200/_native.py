@@ -12,6 +12,9 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmuxflow.so")
+if os.environ.get("MUX_TUNING") == "1" and os.environ.get("MUX_LIB_VARIANT"):
+    # experiment builds (tools/build_variant.py): same sources, other compile-time constants
+    LIB_PATH = os.path.join(_HERE, "..", "tools", "_variants", os.environ["MUX_LIB_VARIANT"] + ".so")
 
 MUX_OK, MUX_EINVAL, MUX_ECUDA, MUX_ENOMEM, MUX_ELIMIT = 0, 1, 2, 3, 4
 MUX_W_F64, MUX_W_F32, MUX_W_I32, MUX_W_I64 = 0, 1, 2, 3

@@ -26,7 +26,7 @@ def _stale():
 OBJDIR = os.path.join(HERE, "build")
 
 
-def _compile(nvcc, src, obj, force):
+def _compile(nvcc, src, obj, force, extra=()):
     """One translation unit -> object (skipped when the object is newer than
     the source and the shared headers)."""
     deps = [src, os.path.join(CSRC, "common.cuh"), os.path.join(HERE, "..", "include", "muxflow.h")]
@@ -34,38 +34,42 @@ def _compile(nvcc, src, obj, force):
         deps.append(os.path.join(CSRC, "ssp.cu"))
     if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj) for d in deps):
         return None
-    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra)
     return subprocess.Popen([nvcc] + flags + ["-c", src, "-o", obj], stdout=subprocess.PIPE,
                             stderr=subprocess.PIPE, text=True)
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, extra=(), out=None, objdir=None):
+    """Build the library; `extra` nvcc flags with their own `out` / `objdir`
+    give experiment variants (tools/build_variant.py)."""
+    out = out or OUT
+    objdir = objdir or OBJDIR
+    if not force and not extra and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    os.makedirs(OBJDIR, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
     for f in SOURCES:
-        obj = os.path.join(OBJDIR, f.replace(".cu", ".o"))
+        obj = os.path.join(objdir, f.replace(".cu", ".o"))
         objs.append(obj)
-        p = _compile(nvcc, os.path.join(CSRC, f), obj, force)
+        p = _compile(nvcc, os.path.join(CSRC, f), obj, force, extra)
         if p is not None:
             procs.append((f, p))
     for f, p in procs:   # translation units compile in parallel
-        out, err = p.communicate()
+        so, se = p.communicate()
         if p.returncode != 0:
-            sys.stderr.write(out + err)
+            sys.stderr.write(so + se)
             raise RuntimeError(f"nvcc failed compiling {f}")
         if verbose:
-            sys.stderr.write(err)
+            sys.stderr.write(se)
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
-           "-o", OUT + ".tmp"] + objs
+           "-o", out + ".tmp"] + objs
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed linking libmuxflow.so")
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

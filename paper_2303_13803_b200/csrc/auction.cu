@@ -1384,7 +1384,7 @@ using namespace mux;
 
 int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t M, int64_t ldw, int32_t n,
                    int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
-                   cudaStream_t st, mux_stats_t* stats);
+                   cudaStream_t st, mux_stats_t* stats, bool exact);
 
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
@@ -1487,7 +1487,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
                 untranspose_duals_kernel<int64_t><<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
                     static_cast<const int64_t*>(WT), ldt, mm, nn, pT, corT, rocT, (int64_t)nn + 1, colr, price, owner);
             if (T.canon)
-                MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, mm, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats));
+                MUX_TRY(mux_canon_impl(ctx, W, wtype, nn, mm, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st, stats, true));
             if (wtype == MUX_W_I32)
                 finalize_ssp_kernel<int32_t><<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(
                     static_cast<const int32_t*>(W), ldw, nn, mm, colr, col_out_dev);
@@ -1518,7 +1518,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
                 // canonicalisation works in the auction's units: benefits Q * (n + 1)
                 scale_price_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(price, nn, (int64_t)nn + 1);
                 MUX_TRY(mux_canon_impl(ctx, W, wtype, (int32_t)N, nn, ldw, nn, (int64_t)nn + 1, 0, price, colr, owner, st,
-                                       stats));
+                                       stats, true));
                 // the canonical assignment has the same (optimal) total
                 if (wtype == MUX_W_I32)
                     finalize_ssp_kernel<int32_t><<<(unsigned)((N + 255) / 256), 256, 0, st>>>(
@@ -1655,7 +1655,7 @@ int mux_match_impl(mux_ctx_t* ctx, const void* W, int wtype, int64_t N, int64_t 
             MUX_CUDA_TRY(cudaMemcpy(&pre, A.cnt, sizeof(pre), cudaMemcpyDeviceToHost));
             if (!(pre.errors & (kErrIterGuard | kErrPriceBits))) {
                 MUX_TRY(mux_canon_impl(ctx, W, wtype, (int32_t)N, (int32_t)M, ldw, (int32_t)n, A.SC, A.qshift,
-                                       A.price, A.col, A.owner, st, stats));
+                                       A.price, A.col, A.owner, st, stats, false));
                 launches += 2;
             }
         }

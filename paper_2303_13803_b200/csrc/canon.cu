@@ -73,6 +73,7 @@ struct CanonArgs {
 
 constexpr uint32_t kCanonErrGuard = 1u << 0;
 constexpr uint32_t kCanonErrCap = 1u << 1;
+constexpr uint32_t kCanonErrDual = 1u << 2;   // a real pair above its row's profit: the duals are not feasible
 constexpr int kCanonThreads = 512;
 
 template <int WT>
@@ -167,7 +168,19 @@ __global__ void __launch_bounds__(kCanonThreads, 1) dual_repair_kernel(CanonArgs
     }
 }
 
+// Row profits u_i = a_i,col(i) * SC - p_col(i) of duals that are already
+// exact (the SSP solver's): the repair sweeps are skipped and the tight
+// kernel's count pass checks feasibility instead.
+template <int WT>
+__global__ void profit_kernel(CanonArgs C) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < C.n; i += gridDim.x * blockDim.x) {
+        const int32_t j = C.col[i];
+        C.u[i] = cq<WT>(C, i, j) * C.SC - C.price[j];
+    }
+}
+
 // Tight edges of every real row, in column order: count, reserve, write.
+// The count pass also flags any pair above its row's profit (kCanonErrDual).
 template <int WT>
 __global__ void __launch_bounds__(256) tight_kernel(CanonArgs C) {
     const int lane = threadIdx.x & 31;
@@ -177,13 +190,18 @@ __global__ void __launch_bounds__(256) tight_kernel(CanonArgs C) {
         const int32_t i = (int32_t)row;
         const int64_t ui = C.u[i];
         int32_t cnt = 0;
+        bool above = false;
         for (int32_t c = lane * 4; c < C.M; c += 128) {
             int64_t q[4];
             cq4<WT>(C, i, c, q);
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (c + t < C.M && q[t] * C.SC - __ldcg(C.price + c + t) == ui) ++cnt;
+            for (int t = 0; t < 4; ++t) {
+                const int64_t v = c + t < C.M ? q[t] * C.SC - __ldcg(C.price + c + t) : INT64_MIN;
+                cnt += v == ui;
+                above |= v > ui;
+            }
         }
+        if (above) atomicOr(&C.cnt->errors, kCanonErrDual);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         long long off = 0;
@@ -244,6 +262,8 @@ struct Canon {
     std::vector<char> locked;
     std::vector<uint32_t> stamp;
     std::vector<int32_t> parent;
+    std::vector<int32_t> frontier, nxt;                  // BFS levels, reused across searches
+    std::vector<std::pair<int32_t, int32_t>> moves;      // the applied path
     uint32_t epoch = 0;
     long long searches = 0;
 
@@ -259,7 +279,8 @@ struct Canon {
         ++searches;
         ++epoch;
         stamp[banned_col] = epoch;
-        std::vector<int32_t> frontier{start_row}, nxt;
+        frontier.assign(1, start_row);
+        nxt.clear();
         bool found = false, z_done = false, zp_done = false;
         auto visit = [&](int32_t r, int32_t j) -> bool {
             if (seen(j)) return false;
@@ -296,7 +317,7 @@ struct Canon {
         }
         if (!found) return false;
         // reconstruct from the target back to start_row, then apply
-        std::vector<std::pair<int32_t, int32_t>> moves;
+        moves.clear();
         int32_t j = target_col;
         for (;;) {
             const int32_t r = parent[j];
@@ -341,7 +362,7 @@ using namespace mux;
 
 int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t M, int64_t ldw, int32_t n,
                    int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
-                   cudaStream_t st, mux_stats_t* stats) {
+                   cudaStream_t st, mux_stats_t* stats, bool exact) {
     if (N <= 0 || M <= 0 || n <= 0) return MUX_OK;
     const auto h0 = std::chrono::steady_clock::now();
     // default tight-edge buffer: ~4 n edges in a predictor round; a round with
@@ -373,52 +394,87 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
     C.ent = reinterpret_cast<int32_t*>(base + o_ent);
     C.cap = cap;
     C.sweep_guard = 4ll * n + 16;
-    MUX_CUDA_TRY(cudaMemsetAsync(C.cnt, 0, sizeof(CanonCounters), st));
 
-    void* fn = wtype == MUX_W_I32 ? (void*)dual_repair_kernel<MUX_W_I32> : (void*)dual_repair_kernel<MUX_W_I64>;
-    int per_sm = 0;
-    MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCanonThreads, 0));
-    if (per_sm < 1) { set_error("dual repair kernel cannot be resident"); return MUX_ECUDA; }
-    void* args[] = {&C};
-    MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)ctx->num_sms), dim3(kCanonThreads), args, 0, st));
     const unsigned tg = (unsigned)std::min<int64_t>(((int64_t)N * 32 + 255) / 256, (int64_t)ctx->num_sms * 8);
-    if (wtype == MUX_W_I32) tight_kernel<MUX_W_I32><<<tg, 256, 0, st>>>(C);
-    else tight_kernel<MUX_W_I64><<<tg, 256, 0, st>>>(C);
-    MUX_CUDA_TRY(cudaGetLastError());
-
-    CanonCounters hc;
-    MUX_CUDA_TRY(cudaMemcpyAsync(&hc, C.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    MUX_CUDA_TRY(cudaStreamSynchronize(st));
-    const auto h1 = std::chrono::steady_clock::now();
-    if (hc.errors & kCanonErrGuard) { set_error("canonicalisation: dual repair did not converge"); return MUX_ELIMIT; }
-    if (hc.errors & kCanonErrCap) {
-        // more tight edges than the default buffer holds (many equal scores):
-        // the count pass already has the exact total -- size for it and rerun
-        const int64_t need = (int64_t)hc.tight_total;
-        if (need > (int64_t)N * (int64_t)M) { set_error("canonicalisation: tight-edge count out of range"); return MUX_ELIMIT; }
-        MUX_TRY(ctx->canon_ent.ensure(4ull * (size_t)need + 256));
-        C.ent = ctx->canon_ent.as<int32_t>();
-        C.cap = need;
-        MUX_CUDA_TRY(cudaMemsetAsync(&C.cnt->tight_total, 0, sizeof(unsigned long long), st));
-        MUX_CUDA_TRY(cudaMemsetAsync(&C.cnt->errors, 0, sizeof(uint32_t), st));
+    auto repair_and_tight = [&](bool repair) -> int {
+        if (repair) {
+            void* fn = wtype == MUX_W_I32 ? (void*)dual_repair_kernel<MUX_W_I32> : (void*)dual_repair_kernel<MUX_W_I64>;
+            int per_sm = 0;
+            MUX_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kCanonThreads, 0));
+            if (per_sm < 1) { set_error("dual repair kernel cannot be resident"); return MUX_ECUDA; }
+            void* args[] = {&C};
+            MUX_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3((unsigned)ctx->num_sms), dim3(kCanonThreads), args, 0, st));
+        } else {
+            const unsigned pg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->num_sms * 4);
+            if (wtype == MUX_W_I32) profit_kernel<MUX_W_I32><<<pg, 256, 0, st>>>(C);
+            else profit_kernel<MUX_W_I64><<<pg, 256, 0, st>>>(C);
+        }
         if (wtype == MUX_W_I32) tight_kernel<MUX_W_I32><<<tg, 256, 0, st>>>(C);
         else tight_kernel<MUX_W_I64><<<tg, 256, 0, st>>>(C);
         MUX_CUDA_TRY(cudaGetLastError());
+        return MUX_OK;
+    };
+    CanonCounters hc;
+    std::vector<int32_t> col(n), rcnt(N), ent;
+    std::vector<int64_t> p(n), u(n), roff(N);
+    // GPU part: profits (+ repair sweeps), tight CSR, copies to the host
+    auto gpu_phase = [&](bool repair) -> int {
+        MUX_CUDA_TRY(cudaMemsetAsync(C.cnt, 0, sizeof(CanonCounters), st));
+        MUX_TRY(repair_and_tight(repair));
         MUX_CUDA_TRY(cudaMemcpyAsync(&hc, C.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
         MUX_CUDA_TRY(cudaStreamSynchronize(st));
-        if (hc.errors & kCanonErrCap) { set_error("canonicalisation: tight-edge graph exceeds its buffer"); return MUX_ELIMIT; }
-    }
-
-    std::vector<int32_t> col(n), rcnt(N), ent((size_t)hc.tight_total);
-    std::vector<int64_t> p(n), u(n), roff(N);
-    MUX_CUDA_TRY(cudaMemcpyAsync(col.data(), col_dev, 4ull * n, cudaMemcpyDeviceToHost, st));
-    MUX_CUDA_TRY(cudaMemcpyAsync(p.data(), price, 8ull * n, cudaMemcpyDeviceToHost, st));
-    MUX_CUDA_TRY(cudaMemcpyAsync(u.data(), C.u, 8ull * n, cudaMemcpyDeviceToHost, st));
-    MUX_CUDA_TRY(cudaMemcpyAsync(rcnt.data(), C.row_cnt, 4ull * N, cudaMemcpyDeviceToHost, st));
-    MUX_CUDA_TRY(cudaMemcpyAsync(roff.data(), C.row_off, 8ull * N, cudaMemcpyDeviceToHost, st));
-    if (hc.tight_total)
-        MUX_CUDA_TRY(cudaMemcpyAsync(ent.data(), C.ent, 4ull * hc.tight_total, cudaMemcpyDeviceToHost, st));
-    MUX_CUDA_TRY(cudaStreamSynchronize(st));
+        if (hc.errors & kCanonErrGuard) { set_error("canonicalisation: dual repair did not converge"); return MUX_ELIMIT; }
+        if (hc.errors & kCanonErrDual) return MUX_OK;   // caller decides (exact duals that were not)
+        if (hc.errors & kCanonErrCap) {
+            // more tight edges than the default buffer holds (many equal scores):
+            // the count pass already has the exact total -- size for it and rerun
+            const int64_t need = (int64_t)hc.tight_total;
+            if (need > (int64_t)N * (int64_t)M) { set_error("canonicalisation: tight-edge count out of range"); return MUX_ELIMIT; }
+            MUX_TRY(ctx->canon_ent.ensure(4ull * (size_t)need + 256));
+            C.ent = ctx->canon_ent.as<int32_t>();
+            C.cap = need;
+            MUX_CUDA_TRY(cudaMemsetAsync(&C.cnt->tight_total, 0, sizeof(unsigned long long), st));
+            MUX_CUDA_TRY(cudaMemsetAsync(&C.cnt->errors, 0, sizeof(uint32_t), st));
+            if (wtype == MUX_W_I32) tight_kernel<MUX_W_I32><<<tg, 256, 0, st>>>(C);
+            else tight_kernel<MUX_W_I64><<<tg, 256, 0, st>>>(C);
+            MUX_CUDA_TRY(cudaGetLastError());
+            MUX_CUDA_TRY(cudaMemcpyAsync(&hc, C.cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+            MUX_CUDA_TRY(cudaStreamSynchronize(st));
+            if (hc.errors & kCanonErrCap) { set_error("canonicalisation: tight-edge graph exceeds its buffer"); return MUX_ELIMIT; }
+        }
+        ent.resize((size_t)hc.tight_total);
+        MUX_CUDA_TRY(cudaMemcpyAsync(col.data(), col_dev, 4ull * n, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(p.data(), price, 8ull * n, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(u.data(), C.u, 8ull * n, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(rcnt.data(), C.row_cnt, 4ull * N, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(roff.data(), C.row_off, 8ull * N, cudaMemcpyDeviceToHost, st));
+        if (hc.tight_total)
+            MUX_CUDA_TRY(cudaMemcpyAsync(ent.data(), C.ent, 4ull * hc.tight_total, cudaMemcpyDeviceToHost, st));
+        MUX_CUDA_TRY(cudaStreamSynchronize(st));
+        return MUX_OK;
+    };
+    // padding rows / columns are implicit in the tight kernel: their feasibility
+    // (a padding row's column has the minimum price; no real row profits below a
+    // padding column's -p) is checked here for duals taken as exact
+    auto padding_feasible = [&]() -> bool {
+        if (N < n) {
+            const int64_t pmin = *std::min_element(p.begin(), p.end());
+            for (int32_t i = N; i < n; ++i)
+                if (p[col[i]] != pmin) return false;
+        }
+        if (M < n) {
+            const int64_t pmin = *std::min_element(p.begin() + M, p.end());
+            for (int32_t i = 0; i < N; ++i)
+                if (u[i] < -pmin) return false;
+        }
+        return true;
+    };
+    // exact duals (the SSP solver's): profits + tight edges only; the repair
+    // sweeps run only if a feasibility check fails
+    MUX_TRY(gpu_phase(!exact));
+    if (exact && ((hc.errors & kCanonErrDual) || !padding_feasible())) MUX_TRY(gpu_phase(true));
+    if (hc.errors & kCanonErrDual) { set_error("canonicalisation: duals infeasible after repair"); return MUX_ELIMIT; }
+    const auto h1 = std::chrono::steady_clock::now();
 
     const auto h2 = std::chrono::steady_clock::now();
     TightGraph G;
@@ -443,7 +499,7 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
         auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
             return std::chrono::duration<double, std::milli>(b - a).count();
         };
-        fprintf(stderr, "[mux] canon: dual repair + tight %.2f ms (%llu sweeps, %llu row scans), D2H %.2f ms, "
+        fprintf(stderr, "[mux] canon: GPU (profits / repair, tight CSR) + D2H %.2f ms (%llu sweeps, %llu row scans), setup %.2f ms, "
                         "host %.2f ms (%lld searches, %llu tight edges)\n",
                 ms(h0, h1), hc.sweeps, hc.row_scans, ms(h1, h2), ms(h2, h3), K.searches, hc.tight_total);
     }

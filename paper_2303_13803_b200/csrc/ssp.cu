@@ -1018,7 +1018,10 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
 // distance in any order, and a relaxation from one of them cannot take another
 // below that distance.  Only matched winners batch (a free winner ends the
 // search; free columns sort first, so none ties with a matched winner).
-constexpr int kTieMax = 3;
+#ifndef MUX_TIE_MAX
+#define MUX_TIE_MAX 3
+#endif
+constexpr int kTieMax = MUX_TIE_MAX;
 struct CTies {
     uint64_t key[2][kTieMax];
     int32_t n[2];
