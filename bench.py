@@ -290,9 +290,9 @@ def run_reference(args, rank, world):
 
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernel from the newest committed ncu capture."""
-    for rnd in ("r02", "r01c", "r01b"):
+    for rnd, name in (("r03", "ncu_rkey_traffic.json"), ("r02", "ncu_cluster_traffic.json")):
         try:
-            with open(os.path.join(ROOT, "profiles", rnd, "ncu_cluster_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", rnd, name)) as f:
                 return json.load(f)["dram_bytes_per_launch"], rnd
         except Exception:
             continue
@@ -514,9 +514,14 @@ def run_ours(args, rank, world, local_rank):
                      "share_of_step": dense_ms / t_step},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": int(s["launches"]),
-        "solver": {k: s[k] for k in ("levels", "par_steps", "dense_steps", "dense_searches", "dense_launches", "ms_dense", "ms_parallel",
-                                     "row_scans", "total_q", "ms_match", "ms_canon", "canon_searches", "tight_edges",
-                                     "dual_sweeps")},
+        "solver": dict({k: s[k] for k in ("levels", "par_steps", "dense_steps", "dense_searches", "dense_launches", "ms_dense",
+                                          "ms_parallel", "row_scans", "total_q", "ms_match", "ms_canon", "canon_searches",
+                                          "tight_edges", "dual_sweeps")},
+                       dense_exchange_steps=s["rounds"],
+                       us_per_pop=1e3 * s["ms_dense"] / max(1, s["dense_steps"]),
+                       us_per_exchange_step=1e3 * s["ms_dense"] / max(1, s["rounds"]),
+                       long_path_sms="8 (one 8-CTA cluster) for levels > 3072 columns, 1 below; scoring and parallel "
+                                     "passes use all SMs"),
         "ms_match": auc_ms, "ms_per_step_all": times,
     }
     if sched_line is not None:

@@ -53,6 +53,7 @@ const Tuning& tuning() {
         t.canon = knob("MUX_CANON", 1, 0, 1, err) == 1;
         t.ssp_rect = knob("MUX_SSP_RECT", 1, 0, 1, err) == 1;
         t.ssp_f = knob("MUX_SSP_F", t.ssp_f, 2, 16, err);
+        t.ssp_fx = getenv("MUX_SSP_FX") ? knob("MUX_SSP_FX", 0, 110, 1600, err) : 0;
         t.ssp_base = knob("MUX_SSP_BASE", t.ssp_base, 8, 4096, err);
         t.ssp_steps = knob("MUX_SSP_STEPS", t.ssp_steps, 1, 100000, err);
         t.ssp_deep = knob("MUX_SSP_DEEP", t.ssp_deep, 0, 1000, err);

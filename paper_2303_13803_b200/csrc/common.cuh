@@ -56,6 +56,7 @@ struct Tuning {
     bool canon = true;           // MUX_CANON=0: skip the tie canonicalisation
     bool ssp_rect = true;        // MUX_SSP_RECT=0: rectangular rounds on the auction
     int ssp_f = 2;               // MUX_SSP_F [2, 16]: coarsening factor between levels
+    int ssp_fx = 0;              // MUX_SSP_FX [110, 1600]: fractional coarsening factor x 100 (0 = MUX_SSP_F)
     int ssp_base = 48;           // MUX_SSP_BASE [8, 4096]: size of the coarsest level
     int ssp_steps = 48;          // MUX_SSP_STEPS [1, 100000]: pops before a warp search is deferred
     int ssp_deep = 4;            // MUX_SSP_DEEP [0, 1000]: dense re-scans before deferral

@@ -2283,11 +2283,17 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     while (lv.back().m > base && price_in == nullptr) {
         const int32_t m = lv.back().m;
         std::vector<int32_t> nr, nc, sub;
-        for (int32_t k = fct / 2; k < m; k += fct) {
+        auto take_k = [&](int32_t k) {
             nr.push_back(cur_r[k]);
             nc.push_back(cur_c[k]);
             // coarse row index within the finer level's row indexing
             sub.push_back(lv.size() == 1 ? cur_r[k] : k);
+        };
+        if (T.ssp_fx > 0) {   // fractional factor fx / 100: evenly spaced strata
+            const int32_t mc = std::max<int32_t>(1, (int32_t)((int64_t)m * 100 / T.ssp_fx));
+            for (int32_t i = 0; i < mc; ++i) take_k((int32_t)(((int64_t)(2 * i + 1) * m) / (2 * (int64_t)mc)));
+        } else {
+            for (int32_t k = fct / 2; k < m; k += fct) take_k(k);
         }
         lv.back().sub = sub;
         LInfo L;
@@ -2689,8 +2695,8 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         ms_levels[l] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tl).count();
         if (verbose)
             fprintf(stderr, "[ssp] level %d m %d: %.3f ms (setup %.3f parallel %.3f) passes %d deferred %d | steps %llu deep %llu aborts %llu "
-                            "augs %llu xsteps %llu xdeep %llu refresh %llu | xcyc pop %.2e deep %.2e step %.2e aug %.2e\n",
-                    l, m, ms_levels[l], ms_setup, ms_par_wall, pass, ndef_total, hc.steps, hc.deep, hc.aborts, hc.augs, hc.xsteps, hc.xdeep,
+                            "augs %llu xsteps %llu xrounds %llu xdeep %llu refresh %llu | xcyc pop %.2e deep %.2e step %.2e aug %.2e\n",
+                    l, m, ms_levels[l], ms_setup, ms_par_wall, pass, ndef_total, hc.steps, hc.deep, hc.aborts, hc.augs, hc.xsteps, hc.xrounds, hc.xdeep,
                     hc.refresh, (double)hc.xcyc[0], (double)hc.xcyc[1], (double)hc.xcyc[2], (double)hc.xcyc[3]);
     }
     // level 0 result
