@@ -1621,6 +1621,89 @@ __device__ __forceinline__ ulonglong2 cluster_min_push2(uint64_t v, uint64_t pay
     return r;
 }
 
+// cluster_min_push2 with tie batching (as cluster_min_push_ties): up to TM
+// further (key, payload) warp minima at the winner's distance, the CLS x NW
+// slots spread over all 32 lanes.
+template <int TM>
+struct CTies2 {
+    ulonglong2 e[2][TM];
+    int32_t n[2];
+};
+
+template <int CLS, int NW, int TM>
+__device__ __forceinline__ ulonglong2 cluster_min_push2_ties(uint64_t v, uint64_t pay, ulonglong2* bres, CPush2<CLS, NW>& P,
+                                                             CTies2<TM>& T, int& par, uint32_t& ph, int rank,
+                                                             ulonglong2 (&te)[TM], int& nt, bool ties) {
+    const uint64_t wv = wmin64(v);
+    const unsigned who = __ballot_sync(0xffffffffu, v == wv);
+    pay = __shfl_sync(0xffffffffu, pay, __ffs(who) - 1);
+    const int w = threadIdx.x >> 5, ln = lane_id();
+    const uint32_t lb = smem_u32(&P.bar[par]);
+    if (ln < CLS) {
+        const uint32_t la = smem_u32(&P.slots[par][rank * 32 + w]);
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(ln));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(ln));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+                     "l"(wv), "l"(pay), "r"(rb)
+                     : "memory");
+    }
+    if (w == 0) {
+        const uint32_t parity = (ph >> par) & 1u;
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(lb), "r"(parity)
+                : "memory");
+        constexpr int TOT = CLS * NW, KPL = (TOT + 31) / 32;
+        ulonglong2 ys[KPL];
+        ulonglong2 x = make_ulonglong2(kNoKey, 0ull);
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const int e = ln + 32 * k;
+            ys[k] = e < TOT ? P.slots[par][(e / NW) * 32 + (e % NW)] : make_ulonglong2(kNoKey, 0ull);
+            if (ys[k].x < x.x) x = ys[k];
+        }
+        const uint64_t m2 = wmin64(x.x);
+        const unsigned h = __ballot_sync(0xffffffffu, x.x == m2);
+        const uint64_t p2 = __shfl_sync(0xffffffffu, x.y, __ffs(h) - 1);
+        const bool batch = ties && (m2 & kFreeBit) != 0 && m2 != kNoKey;
+        const uint64_t dhi = m2 >> kSH;
+        const unsigned lt = (1u << ln) - 1u;
+        int cnt = 0;
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) {
+            const bool tie = batch && (ys[k].x >> kSH) == dhi && ys[k].x != m2;
+            const unsigned msk = __ballot_sync(~0u, tie);
+            if (tie) {
+                const int pos = cnt + __popc(msk & lt);
+                if (pos < TM) T.e[par][pos] = ys[k];
+            }
+            cnt += __popc(msk);
+        }
+        if (ln == 0) {
+            bres[par] = make_ulonglong2(m2, p2);
+            T.n[par] = cnt < TM ? cnt : TM;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CLS * NW * 16) : "memory");
+        }
+    }
+    ph ^= 1u << par;
+    __syncthreads();
+    const ulonglong2 r = bres[par];
+    nt = ties ? T.n[par] : 0;
+    ulonglong2 raw[TM];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) raw[t] = T.e[par][t];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) te[t] = t < nt ? raw[t] : make_ulonglong2(kNoKey, 0ull);
+    par ^= 1;
+    return r;
+}
+
+constexpr int kTieMaxSlice = 1;   // the slice kernel's register budget (512 threads, up to 16 columns each)
+
 template <int CC, int CLS, int NT>
 __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1)
 ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
@@ -1629,6 +1712,10 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
     long long wcyc = 0, scyc = 0;
     __shared__ __align__(16) CPush2<CLS, NW> P;
     __shared__ __align__(16) ulonglong2 bres[2];
+    __shared__ __align__(16) CTies2<kTieMaxSlice> TS;
+    constexpr int TM = kTieMaxSlice;
+    ulonglong2 te[TM];
+    int nt = 0;
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* pred = reinterpret_cast<int32_t*>(smem);   // [mc] predecessor rows (local)
     cg::cluster_group cluster = cg::this_cluster();
@@ -1640,8 +1727,9 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
     const int tid = threadIdx.x;
     int par = 0;
     uint32_t ph = 0;
-    unsigned long long steps = 0;
+    unsigned long long steps = 0, rounds = 0;
     const bool tm = (flags & 16) != 0;
+    const bool ties = (flags & 64) != 0;
     long long tcyc[3] = {0, 0, 0};
     cpush2_init<CLS, NW>(P);
     cluster.sync();
@@ -1673,7 +1761,9 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                 pk[u] = kTop;
             }
         }
-        const ulonglong2 r0 = cluster_min_push2<CLS, NW>(vmin, vpay, bres, P, par, ph, rank);
+        const ulonglong2 r0 = cluster_min_push2_ties<CLS, NW, TM>(vmin, vpay, bres, P, TS, par, ph, rank, te, nt, ties);
+#pragma unroll
+        for (int t = 0; t < TM; ++t) te[t].x &= kLowMask;   // ties at distance 0
         const int64_t pis = -((int64_t)(r0.x >> kSH) - kDistLim);
 #pragma unroll
         for (int u = 0; u < CC; ++u) {
@@ -1692,7 +1782,7 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
             const int32_t i = (int32_t)(bpay & kLowMask) - 1;
             const int64_t pjm = (int64_t)(bpay >> kSH);
             if (i < 0) { jf = jm; D = dmin; break; }
-            if (pop_limit > 0 && ++pops > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
             const long long tA = tm ? clock64() : 0;
             const wt_t* Ai = rowp(L, i);
             wt_t av[CC];
@@ -1702,10 +1792,35 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                 av[u] = jj < nloc ? __ldg(Ai + c0 + jj) : 0;
             }
             const int64_t aim = (int64_t)__ldg(Ai + jm);
+            // tied columns (matched): owner row and price travel in the payload
+            wt_t avt[TM][CC];
+            wt_t aimt[TM];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                if (t < nt) {
+                    const int32_t it = (int32_t)(te[t].y & kLowMask) - 1;
+                    const wt_t* At = rowp(L, it);
+                    aimt[t] = __ldg(At + (int32_t)(te[t].x & kIdxMask));
+#pragma unroll
+                    for (int u = 0; u < CC; ++u) {
+                        const int32_t jj = tid + u * NT;
+                        avt[t][u] = jj < nloc ? __ldg(At + c0 + jj) : 0;
+                    }
+                }
+            }
             if (jm >= c0 && jm < c0 + nloc) {
 #pragma unroll
                 for (int u = 0; u < CC; ++u)
                     if (jm - c0 == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+            }
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                const int32_t jt = (int32_t)(te[t].x & kIdxMask) - c0;
+                if (t < nt && jt >= 0 && jt < nloc) {
+#pragma unroll
+                    for (int u = 0; u < CC; ++u)
+                        if (jt == tid + u * NT) { kd[u] |= kTop; pk[u] |= kTop; }
+                }
             }
             const uint64_t base = (uint64_t)(dmin + aim - pjm) << kSH;
             best = kNoKey;
@@ -1714,10 +1829,26 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
             for (int u = 0; u < CC; ++u) {
                 const uint64_t nk = base + pk[u] - ((uint64_t)av[u] << kSH);
                 if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = i; }
-                if (kd[u] < best) { best = kd[u]; pay = ((pk[u] & ~kTop) & ~kLowMask) | (uint32_t)(own[u] + 1); }
             }
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                if (t < nt) {
+                    const int32_t it = (int32_t)(te[t].y & kLowMask) - 1;
+                    const uint64_t b = (uint64_t)(dmin + (int64_t)aimt[t] - (int64_t)(te[t].y >> kSH)) << kSH;
+#pragma unroll
+                    for (int u = 0; u < CC; ++u) {
+                        const uint64_t nk = b + pk[u] - ((uint64_t)avt[t][u] << kSH);
+                        if (tid + u * NT < nloc && nk < kd[u]) { kd[u] = nk; pred[tid + u * NT] = it; }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < CC; ++u)
+                if (kd[u] < best) { best = kd[u]; pay = ((pk[u] & ~kTop) & ~kLowMask) | (uint32_t)(own[u] + 1); }
+            steps += nt;
+            ++rounds;
             const long long tB = tm ? clock64() : 0;
-            const ulonglong2 r = cluster_min_push2<CLS, NW>(best, pay, bres, P, par, ph, rank);
+            const ulonglong2 r = cluster_min_push2_ties<CLS, NW, TM>(best, pay, bres, P, TS, par, ph, rank, te, nt, ties);
             best = r.x;
             bpay = r.y;
             if (tm) {
@@ -1758,7 +1889,10 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
         cluster.sync();
         if (tm) scyc += clock64() - ts;
     }
-    if (rank == 0 && tid == 0) atomicAdd(&L.cnt->xsteps, steps);
+    if (rank == 0 && tid == 0) {
+        atomicAdd(&L.cnt->xsteps, steps);
+        atomicAdd(&L.cnt->xrounds, rounds);
+    }
     if (tm && rank == 0 && tid == 0) {
         for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
         atomicAdd(&L.cnt->xwalk, walk);

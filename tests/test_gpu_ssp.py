@@ -220,15 +220,18 @@ def test_rectangular_random_vs_lsa(cuda, certified, n, m, hi, seed):
     _check_assignment(Q, col, total)
 
 
-def test_rectangular_sharded_cluster_tables(cuda, certified, monkeypatch):
-    """m above the replicated-table limit (16,384 columns) uses column-sharded
-    cluster tables with per-step DSMEM fetches of the winner's owner and price."""
+@pytest.mark.parametrize("ties", ["1", "0"])
+def test_rectangular_sharded_cluster_tables(cuda, certified, monkeypatch, ties):
+    """m above the replicated-table limit (16,384 columns) runs the slice
+    kernel (ssp_rkey_slice_kernel: owner and price travel with each warp
+    minimum), with and without tie batching; same optimum as the auction."""
     from paper_2303_13803_b200 import default_table, round_arrays
     from paper_2303_13803_b200.synth import make_cluster
     t = default_table()
     cl = make_cluster(1200, 20000, seed=5)
-    col, total, st = round_arrays(t, cl.x, cl.share, cl.y, qbits=20, stats=True)
     monkeypatch.setenv("MUX_TUNING", "1")
+    monkeypatch.setenv("MUX_SSP_TIES", ties)
+    col, total, st = round_arrays(t, cl.x, cl.share, cl.y, qbits=20, stats=True)
     monkeypatch.setenv("MUX_SOLVER", "auction")
     _, t_auc = round_arrays(t, cl.x, cl.share, cl.y, qbits=20)
     assert total == t_auc
