@@ -2670,6 +2670,20 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
             const int32_t mcl = (m + CL - 1) / CL;
             const size_t cl_bytes = (size_t)CBYTES * mcl + 64;
             const int32_t pl = l == 0 ? 0 : coarse_pops;
+            if (T.ssp_dorder && ndef_total > 1) {
+                // long searches in row-key order (default ascending): in these near-monotone
+                // assignments each search shifts a chain of rows toward a free column, and
+                // taking the insertions in key order keeps later chains from re-shifting
+                // earlier ones (10k rounds: 31k -> 26k pops; 4k: 16.5k -> 10.1k)
+                std::vector<int32_t> hd(ndef_total);
+                MUX_CUDA_TRY(cudaMemcpyAsync(hd.data(), L.defer, 4ull * ndef_total, cudaMemcpyDeviceToHost, st));
+                MUX_CUDA_TRY(cudaStreamSynchronize(st));
+                auto key = [&](int32_t r) { return l == 0 ? rk[r] : (double)r; };   // levels >= 1 index rows in key order
+                std::stable_sort(hd.begin(), hd.end(), [&](int32_t a, int32_t b) {
+                    return T.ssp_dorder == 1 ? key(a) < key(b) : key(a) > key(b);
+                });
+                MUX_CUDA_TRY(cudaMemcpyAsync(L.defer, hd.data(), 4ull * ndef_total, cudaMemcpyHostToDevice, st));
+            }
             if (T.ssp_dump) {
                 // analysis dump: header {m, nreal, ndef, level}, A rows [nreal][m], p, roc, cor, defer
                 static int seq = 0;
