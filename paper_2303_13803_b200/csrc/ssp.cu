@@ -2635,6 +2635,13 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         int32_t ndef_total = 0;
         const auto tl2 = std::chrono::steady_clock::now();
         MUX_CUDA_TRY(cudaEventRecord(ev[0], st));
+        if (m <= T.ssp_seq && nlist > 0) {
+            // tiny level: every row goes straight to the sequential long-path kernel
+            // (warps would mostly abort each other on a few dozen columns)
+            MUX_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int32_t*>(B + o_de[l]), list, 4ull * nlist, cudaMemcpyDeviceToDevice, st));
+            ndef_total = nlist;
+            nlist = 0;
+        }
         while (nlist > 0) {
             L.in = list;
             L.nin = nlist;
