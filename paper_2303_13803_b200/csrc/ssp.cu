@@ -2643,6 +2643,14 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
             nlist = 0;
         }
         while (nlist > 0) {
+            if (pass > 0 && nlist <= T.ssp_taildef) {
+                // a handful of retried rows: straight to the long-path kernel, which pops
+                // as fast as a lone warp and never throws a budget-capped search away
+                MUX_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<int32_t*>(B + o_de[l]) + ndef_total, list, 4ull * nlist,
+                                             cudaMemcpyDeviceToDevice, st));
+                ndef_total += nlist;
+                break;
+            }
             L.in = list;
             L.nin = nlist;
             L.retry = bufs[pass & 1];
