@@ -6,6 +6,8 @@ MUX_SSP_CHECK=1 the library also verifies the dense dual certificate
 pi_i + p_j >= a_ij (tight on the matching) at every level, which proves
 optimality independently of any oracle."""
 
+import functools
+
 import numpy as np
 import pytest
 
@@ -127,6 +129,25 @@ def test_level_structure_variants(cuda, certified, tuning, monkeypatch, f, base)
     cl, Q = _pred_Q(1200, 30, 30)
     _, total = _match(Q, keys=(cl.x, cl.y))
     assert total == _lsa(Q)
+
+
+@pytest.mark.parametrize("env", [{"MUX_SSP_DORDER": "0"}, {"MUX_SSP_DORDER": "2"}, {"MUX_SSP_SEQ": "0"},
+                                 {"MUX_SSP_SEQ": "700"}, {"MUX_SSP_TAILDEF": "0"}, {"MUX_SSP_TAILDEF": "64"},
+                                 {"MUX_SSP_FX": "150"}])
+def test_scheduling_variants(cuda, certified, tuning, monkeypatch, env):
+    """Long-search order, the small-level sequential cut-off, the tail hand-off
+    and a fractional level factor change only the work, never the optimum."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cl, Q, want = _pred_case_3000()
+    _, total = _match(Q, keys=(cl.x, cl.y))
+    assert total == want, env
+
+
+@functools.lru_cache(maxsize=1)
+def _pred_case_3000():
+    cl, Q = _pred_Q(3000, 31, 30)
+    return cl, Q, _lsa(Q)
 
 
 def test_long_path_kernels_agree(cuda, certified, tuning, monkeypatch):
