@@ -2532,6 +2532,35 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<10, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<CCOLS, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
+    // 16-CTA clusters for the slice kernel when the device can co-schedule them
+    bool wide_ok = false;
+    static int wide_cache = -1;   // the occupancy query is answered once per process
+    if (T.ssp_wide && wide_cache >= 0) {
+        wide_ok = wide_cache == 1;
+    } else if (T.ssp_wide) {
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, 16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, 16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, 16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = 64 * 1024;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        wide_ok = cudaOccupancyMaxActiveClusters(&nclusters, ssp_rkey_slice_kernel<10, 16, 512>, &cfg) == cudaSuccess &&
+                  nclusters >= 1;
+        cudaGetLastError();   // a refused query only disables the wide clusters
+        wide_cache = wide_ok ? 1 : 0;
+    }
     // register-key kernel flags: 4 = runner-up row prefetch into shared memory, 16 = per-pop cycle timing
     const int32_t cpush = (T.ssp_pf ? 4 : 0) | (T.ssp_time ? 16 : 0) | (T.ssp_l2pf ? 32 : 0) | (T.ssp_ties ? 64 : 0);
     const bool use_cluster = T.ssp_cluster;
@@ -2767,7 +2796,15 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
             } else if (use_cluster && T.ssp_rslice > 0 && mcl <= 512 * 16) {
                 // register keys with (key, owner | price) pushes: no replicated tables
                 const size_t rs_bytes = 4ull * mcl + 64;
-                if (mcl <= 512 * 3) ssp_rkey_slice_kernel<3, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
+                const int32_t m16 = (m + 15) / 16;
+                if (wide_ok && m16 <= 512 * 10) {
+                    // 16-CTA clusters (non-portable size): half the columns per CTA
+                    // (10k x 40k: 156 -> 143 ms of long paths, profiles/r03/cluster16_slice.log)
+                    const size_t rs16 = 4ull * m16 + 64;
+                    if (m16 <= 512 * 3) ssp_rkey_slice_kernel<3, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, cpush);
+                    else if (m16 <= 512 * 6) ssp_rkey_slice_kernel<6, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, cpush);
+                    else ssp_rkey_slice_kernel<10, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, cpush);
+                } else if (mcl <= 512 * 3) ssp_rkey_slice_kernel<3, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 512 * 6) ssp_rkey_slice_kernel<6, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
                 else if (mcl <= 512 * 10) ssp_rkey_slice_kernel<10, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
                 else ssp_rkey_slice_kernel<16, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
