@@ -71,6 +71,7 @@ const Tuning& tuning() {
         t.ssp_ct1 = knob("MUX_SSP_CT1", t.ssp_ct1, 512, 1024, err);
         if (t.ssp_ct1 != 512 && t.ssp_ct1 != 1024 && err.empty()) err = "MUX_SSP_CT1 must be 512 or 1024";
         t.ssp_dump = getenv("MUX_SSP_DUMP");
+        t.canon_dump = getenv("MUX_CANON_DUMP");
         t.ssp_seq = knob("MUX_SSP_SEQ", t.ssp_seq, 0, 4096, err);
         t.ssp_wide = knob("MUX_SSP_WIDE", t.ssp_wide ? 1 : 0, 0, 1, err) == 1;
         t.ssp_taildef = knob("MUX_SSP_TAILDEF", t.ssp_taildef, 0, 4096, err);

@@ -241,124 +241,14 @@ __global__ void __launch_bounds__(256) tight_kernel(CanonArgs C) {
     }
 }
 
-// ---- host: the reference's canonicalisation loop on the sparse tight graph --
-
-namespace {
-
-struct TightGraph {
-    int32_t N, M, n;
-    const std::vector<int32_t>* ent;
-    const std::vector<int32_t>* cnt;
-    const std::vector<int64_t>* off;
-    std::vector<int32_t> Z;       // columns tight to every padding row (N < M)
-    std::vector<int32_t> Zpad;    // padding columns tight to rows with padrow_tight (N > M)
-    std::vector<char> padrow_tight;
-};
-
-struct Canon {
-    const TightGraph& G;
-    std::vector<int32_t>& col;
-    std::vector<int32_t> row_of_col;
-    std::vector<char> locked;
-    std::vector<uint32_t> stamp;
-    std::vector<int32_t> parent;
-    std::vector<int32_t> frontier, nxt;                  // BFS levels, reused across searches
-    std::vector<std::pair<int32_t, int32_t>> moves;      // the applied path
-    uint32_t epoch = 0;
-    long long searches = 0;
-
-    Canon(const TightGraph& g, std::vector<int32_t>& c)
-        : G(g), col(c), row_of_col(g.n), locked(g.n, 0), stamp(g.n, 0), parent(g.n, -1) {
-        for (int32_t i = 0; i < G.n; ++i) row_of_col[col[i]] = i;
-    }
-    bool seen(int32_t j) const { return stamp[j] == epoch || locked[j]; }
-
-    // matching.py:104-145: breadth-first search over tight edges for an
-    // alternating path start_row -> ... -> target_col; applies it on success.
-    bool repair(int32_t start_row, int32_t target_col, int32_t banned_row, int32_t banned_col) {
-        ++searches;
-        ++epoch;
-        stamp[banned_col] = epoch;
-        frontier.assign(1, start_row);
-        nxt.clear();
-        bool found = false, z_done = false, zp_done = false;
-        auto visit = [&](int32_t r, int32_t j) -> bool {
-            if (seen(j)) return false;
-            stamp[j] = epoch;
-            parent[j] = r;
-            if (j == target_col) return true;
-            const int32_t r2 = row_of_col[j];
-            if (r2 != banned_row) nxt.push_back(r2);
-            return false;
-        };
-        while (!frontier.empty() && !found) {
-            nxt.clear();
-            for (int32_t r : frontier) {
-                if (r >= G.N) {                      // padding row: tight to Z
-                    if (!z_done) {
-                        z_done = true;   // every later padding row finds Z visited
-                        for (int32_t j : G.Z)
-                            if (visit(r, j)) { found = true; break; }
-                    }
-                } else {
-                    const int32_t* e = G.ent->data() + (*G.off)[r];
-                    const int32_t k = (*G.cnt)[r];
-                    for (int32_t t = 0; t < k && !found; ++t)
-                        if (visit(r, e[t] & 0x7fffffff)) found = true;
-                    if (!found && G.padrow_tight.size() && G.padrow_tight[r] && !zp_done) {
-                        zp_done = true;
-                        for (int32_t j : G.Zpad)
-                            if (visit(r, j)) { found = true; break; }
-                    }
-                }
-                if (found) break;
-            }
-            frontier.swap(nxt);
-        }
-        if (!found) return false;
-        // reconstruct from the target back to start_row, then apply
-        moves.clear();
-        int32_t j = target_col;
-        for (;;) {
-            const int32_t r = parent[j];
-            moves.emplace_back(r, j);
-            if (r == start_row) break;
-            j = col[r];
-        }
-        for (auto& m : moves) { row_of_col[m.second] = m.first; col[m.first] = m.second; }
-        return true;
-    }
-
-    // matching.py:173-199
-    void run() {
-        for (int32_t i = 0; i < G.N; ++i) {
-            int32_t j_cur = col[i];
-            const int32_t* e = G.ent->data() + (*G.off)[i];
-            const int32_t k = (*G.cnt)[i];
-            bool emitted = false;
-            if (j_cur < G.M)
-                for (int32_t t = 0; t < k; ++t)
-                    if ((e[t] & 0x7fffffff) == j_cur) { emitted = (e[t] >= 0); break; }
-            for (int32_t t = 0; t < k; ++t) {
-                if (e[t] < 0) continue;                 // zero weight
-                const int32_t j = e[t];
-                if (locked[j]) continue;
-                if (emitted && j >= j_cur) break;
-                if (!repair(row_of_col[j], j_cur, i, j)) continue;
-                row_of_col[j] = i;
-                col[i] = j;
-                j_cur = j;
-                break;
-            }
-            locked[j_cur] = 1;
-        }
-    }
-};
-
-}  // namespace
 }  // namespace mux
 
+#include "canon_host.h"
+
+
 using namespace mux;
+using mux::canon_host::Canon;
+using mux::canon_host::TightGraph;
 
 int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t M, int64_t ldw, int32_t n,
                    int64_t SC, int32_t qshift, int64_t* price, int32_t* col_dev, const int32_t* owner,
@@ -492,9 +382,28 @@ int mux_canon_impl(mux_ctx_t* ctx, const void* W, int wtype, int32_t N, int32_t 
         G.padrow_tight.assign(N, 0);
         for (int32_t i = 0; i < N; ++i) G.padrow_tight[i] = (-u[i] == pmin);
     }
+    std::vector<int32_t> col_in;
+    if (tuning().canon_dump) col_in = col;
     Canon K(G, col);
     K.run();
     const auto h3 = std::chrono::steady_clock::now();
+    if (tuning().canon_dump) {
+        // analysis dump for tools/canon_host_bench.cpp: the host loop's inputs and output
+        if (FILE* f = fopen(tuning().canon_dump, "wb")) {
+            const int32_t hdr[7] = {N, M, n, (int32_t)ent.size(), (int32_t)G.Z.size(), (int32_t)G.Zpad.size(),
+                                    (int32_t)G.padrow_tight.size()};
+            fwrite(hdr, 4, 7, f);
+            fwrite(col_in.data(), 4, n, f);
+            fwrite(rcnt.data(), 4, N, f);
+            fwrite(roff.data(), 8, N, f);
+            fwrite(ent.data(), 4, ent.size(), f);
+            fwrite(G.Z.data(), 4, G.Z.size(), f);
+            fwrite(G.Zpad.data(), 4, G.Zpad.size(), f);
+            fwrite(G.padrow_tight.data(), 1, G.padrow_tight.size(), f);
+            fwrite(col.data(), 4, n, f);
+            fclose(f);
+        }
+    }
     if (tuning().verbose) {
         auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
             return std::chrono::duration<double, std::milli>(b - a).count();
