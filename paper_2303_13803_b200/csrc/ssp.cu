@@ -44,6 +44,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 #include <vector>
 
@@ -2361,6 +2362,36 @@ using namespace mux::ssp64;
 
 static size_t al256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// Indices 0..n-1 in ascending key order, equal keys in index order: the order
+// std::stable_sort gives with `<`, by an LSD radix sort on the keys' ordered
+// bit patterns (8 passes of 8 bits; -0.0 is folded into +0.0 first, keys
+// are never NaN).
+static void key_order(const std::vector<double>& key, std::vector<int32_t>& idx) {
+    const size_t n = key.size();
+    std::vector<uint64_t> k(n), k2(n);
+    std::vector<int32_t> i2(n);
+    for (size_t t = 0; t < n; ++t) {
+        const double v = key[t] == 0.0 ? 0.0 : key[t];
+        uint64_t b;
+        memcpy(&b, &v, 8);
+        k[t] = (b >> 63) ? ~b : (b | (1ull << 63));
+        idx[t] = (int32_t)t;
+    }
+    for (int sh = 0; sh < 64; sh += 8) {
+        size_t cnt[257] = {0};
+        for (size_t t = 0; t < n; ++t) ++cnt[((k[t] >> sh) & 255) + 1];
+        if (cnt[((k[0] >> sh) & 255) + 1] == n) continue;   // one bucket: the pass keeps the order
+        for (int b = 0; b < 256; ++b) cnt[b + 1] += cnt[b];
+        for (size_t t = 0; t < n; ++t) {
+            const size_t d = cnt[(k[t] >> sh) & 255]++;
+            k2[d] = k[t];
+            i2[d] = idx[t];
+        }
+        k.swap(k2);
+        idx.swap(i2);
+    }
+}
+
 // Multilevel exact solve of the square int32 problem W [n][ldw].
 // rowkey / colkey: host ordering keys (may be null: row / column sums).
 // price_out (device int64 [n], optional): optimal column prices (max form).
@@ -2405,8 +2436,8 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     std::vector<int32_t> ro(n), co(n);
     std::iota(ro.begin(), ro.end(), 0);
     std::iota(co.begin(), co.end(), 0);
-    std::stable_sort(ro.begin(), ro.end(), [&](int32_t a, int32_t b) { return rk[a] < rk[b]; });
-    std::stable_sort(co.begin(), co.end(), [&](int32_t a, int32_t b) { return ck[a] < ck[b]; });
+    key_order(rk, ro);
+    key_order(ck, co);
 
     // level hierarchy: level 0 = all (original order); level l+1 = every f-th of level l's sorted order
     struct LInfo { int32_t m; std::vector<int32_t> rows, cols, sub; int32_t plo = 0, phi = 0; };
