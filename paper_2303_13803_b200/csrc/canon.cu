@@ -183,36 +183,69 @@ __global__ void profit_kernel(CanonArgs C) {
 // The count pass also flags any pair above its row's profit (kCanonErrDual).
 template <int WT>
 __global__ void __launch_bounds__(256) tight_kernel(CanonArgs C) {
+    // one read of each row: its tight entries are gathered in column order in
+    // shared memory (kTightBuf per warp) and written out once the row's offset
+    // is known; a row with more tight entries reads itself a second time
+    constexpr int kTightBuf = 256;
+    __shared__ int32_t sbuf[8][kTightBuf];
+    int32_t* buf = sbuf[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t row = gw; row < C.N; row += nw) {
         const int32_t i = (int32_t)row;
         const int64_t ui = C.u[i];
-        int32_t cnt = 0;
+        int32_t base = 0;
         bool above = false;
-        for (int32_t c = lane * 4; c < C.M; c += 128) {
-            int64_t q[4];
-            cq4<WT>(C, i, c, q);
+        for (int32_t c0 = 0; c0 < C.M; c0 += 128) {
+            const int32_t c = c0 + lane * 4;
+            int64_t q[4] = {0, 0, 0, 0};
+            bool tq[4] = {false, false, false, false};
+            int32_t mine = 0;
+            if (c < C.M) {
+                cq4<WT>(C, i, c, q);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const int64_t v = c + t < C.M ? q[t] * C.SC - __ldcg(C.price + c + t) : INT64_MIN;
-                cnt += v == ui;
-                above |= v > ui;
+                for (int t = 0; t < 4; ++t) {
+                    const int64_t v = c + t < C.M ? q[t] * C.SC - __ldcg(C.price + c + t) : INT64_MIN;
+                    tq[t] = v == ui;
+                    above |= v > ui;
+                    mine += tq[t];
+                }
             }
+            if (__ballot_sync(0xffffffffu, mine > 0) == 0u) continue;
+            int32_t incl = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            int32_t pos = base + incl - mine;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (tq[t]) {
+                    if (pos < kTightBuf) buf[pos] = (c + t) | (q[t] == 0 ? (int32_t)0x80000000 : 0);
+                    ++pos;
+                }
+            base += __shfl_sync(0xffffffffu, incl, 31);
         }
         if (above) atomicOr(&C.cnt->errors, kCanonErrDual);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        const int32_t cnt = base;
         long long off = 0;
         if (lane == 0) off = (long long)atomicAdd(&C.cnt->tight_total, (unsigned long long)cnt);
         off = __shfl_sync(0xffffffffu, off, 0);
         if (lane == 0) { C.row_cnt[i] = cnt; C.row_off[i] = off; }
+        __syncwarp();
         if (off + cnt > C.cap) {
             if (lane == 0) atomicOr(&C.cnt->errors, kCanonErrCap);
             continue;
         }
-        int32_t base = 0;
+        if (cnt <= kTightBuf) {
+            for (int32_t t = lane; t < cnt; t += 32) C.ent[off + t] = buf[t];
+            __syncwarp();
+            continue;
+        }
+        // many equal scores: a second read of the row writes its entries directly
+        int32_t b2 = 0;
         for (int32_t c0 = 0; c0 < C.M; c0 += 128) {
             const int32_t c = c0 + lane * 4;
             int64_t q[4] = {0, 0, 0, 0};
@@ -232,11 +265,11 @@ __global__ void __launch_bounds__(256) tight_kernel(CanonArgs C) {
                 const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            int32_t pos = base + incl - mine;
+            int32_t pos = b2 + incl - mine;
 #pragma unroll
             for (int t = 0; t < 4; ++t)
                 if (tq[t]) C.ent[off + pos++] = (c + t) | (q[t] == 0 ? (int32_t)0x80000000 : 0);
-            base += __shfl_sync(0xffffffffu, incl, 31);
+            b2 += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
 }
