@@ -520,7 +520,7 @@ def run_ours(args, rank, world, local_rank):
                        dense_exchange_steps=s["rounds"],
                        us_per_pop=1e3 * s["ms_dense"] / max(1, s["dense_steps"]),
                        us_per_exchange_step=1e3 * s["ms_dense"] / max(1, s["rounds"]),
-                       long_path_sms="8 (one 8-CTA cluster) for levels > 3072 columns, 1 below; scoring and parallel "
+                       long_path_sms="8 (one 8-CTA cluster) for levels > 1300 columns, 1 below; scoring and parallel "
                                      "passes use all SMs"),
         "ms_match": auc_ms, "ms_per_step_all": times,
     }

@@ -76,7 +76,7 @@ struct Tuning {
     int ssp_dorder = 1;          // MUX_SSP_DORDER [0, 2]: long searches in defer order / ascending / descending row key
     const char* ssp_dump = nullptr;
     const char* canon_dump = nullptr;   // MUX_CANON_DUMP=file: the canonicalisation host loop's inputs and output   // MUX_SSP_DUMP=dir: write each long-search batch's level state (analysis)
-    int ssp_one = 2560;          // MUX_SSP_ONE [0, 10240]: levels up to this size run long paths on one SM
+    int ssp_one = 1300;          // MUX_SSP_ONE [0, 10240]: levels up to this size run long paths on one SM
     int auc_theta = 4;           // MUX_THETA [2, 64]: epsilon-scaling factor
     int auc_tail = -1;           // MUX_TAIL [-1, 2^20]: unassigned count that ends the Jacobi rounds (clamped to 16)
     int auc_k = 15;              // MUX_K [1, 15]: cached candidates per bidder
