@@ -510,7 +510,7 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "traffic_note": f"DRAM read+write bytes per launch (ncu --set full, profiles/{traffic_src})",
                      "algorithmic_bytes": dense_bytes, "kernel_ms": dense_ms,
                      "algorithmic_bytes_per_launch": dense_bytes / max(1.0, sum(x["dense_launches"] for x in stats_all) / len(stats_all)),
-                     "note": "latency-bound: one cluster exchange per Dijkstra step (a step pops the minimum plus up to 3 tied warp minima); bytes = 4*m per pop",
+                     "note": "latency-bound: one cluster exchange per Dijkstra step (a step pops the minimum plus up to 2 tied warp minima); bytes = 4*m per pop",
                      "share_of_step": dense_ms / t_step},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
         "gpu_launches": int(s["launches"]),

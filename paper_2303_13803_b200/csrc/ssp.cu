@@ -1020,7 +1020,7 @@ __device__ __forceinline__ uint64_t cluster_min_push(uint64_t v, CShared& S, CPu
 // below that distance.  Only matched winners batch (a free winner ends the
 // search; free columns sort first, so none ties with a matched winner).
 #ifndef MUX_TIE_MAX
-#define MUX_TIE_MAX 3
+#define MUX_TIE_MAX 2
 #endif
 constexpr int kTieMax = MUX_TIE_MAX;
 struct CTies {
