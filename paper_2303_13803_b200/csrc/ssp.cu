@@ -1348,21 +1348,15 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             const int32_t jm = (int32_t)(best & kIdxMask);
             const int64_t dmin = (int64_t)(best >> kSH);
             const int32_t i = rocr[jm];
-            if (i < 0) { jf = jm; D = dmin; break; }
-            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (rank == 0 && tid == 0) {
-                colof[i] = jm;
-#pragma unroll
-                for (int t = 0; t < kTieMax; ++t)
-                    if (t < nt) colof[rocr[tk[t] & kIdxMask]] = (int32_t)(tk[t] & kIdxMask);
-            }
+            // this step's row loads go out first (a free winner, i < 0, ends the search
+            // below; its loads read the zero row); the bookkeeping follows them
             const long long tA = tm ? clock64() : 0;
-            const wt_t* Ai = rowp(L, i);
+            const wt_t* Ai = i >= 0 ? rowp(L, i) : L.zrow;
             const int64_t aim = (int64_t)__ldg(Ai + jm);
             wt_t av[CC];
             // the runner-up of the previous step has its slice (being) copied into smem;
             // its barrier is waited on only after every global load of this step is issued
-            const bool hit = pf && pfrow[cur] == i;
+            const bool hit = pf && i >= 0 && pfrow[cur] == i;
             if (!hit) {
 #pragma unroll
                 for (int u = 0; u < CC; ++u) {
@@ -1388,6 +1382,15 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                         avt[t][u] = jj < nloc ? __ldg(At + c0 + jj) : 0;
                     }
                 }
+            }
+            asm volatile("" ::: "memory");
+            if (i < 0) { jf = jm; D = dmin; break; }
+            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (rank == 0 && tid == 0) {
+                colof[i] = jm;
+#pragma unroll
+                for (int t = 0; t < kTieMax; ++t)
+                    if (t < nt) colof[it[t]] = (int32_t)(tk[t] & kIdxMask);
             }
             // runner-up prefetch: warp 0 copies this CTA's slice of the row owning the
             // runner-up column (often the next pop) into the other buffer by TMA
