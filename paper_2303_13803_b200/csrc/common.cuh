@@ -58,7 +58,7 @@ struct Tuning {
     int ssp_f = 2;               // MUX_SSP_F [2, 16]: coarsening factor between levels
     int ssp_fx = 0;              // MUX_SSP_FX [110, 1600]: fractional coarsening factor x 100 (0 = MUX_SSP_F)
     int ssp_base = 48;           // MUX_SSP_BASE [8, 4096]: size of the coarsest level
-    int ssp_steps = 48;          // MUX_SSP_STEPS [1, 100000]: pops before a warp search is deferred
+    int ssp_steps = 24;          // MUX_SSP_STEPS [1, 100000]: pops before a warp search is deferred
     int ssp_deep = 4;            // MUX_SSP_DEEP [0, 1000]: dense re-scans before deferral
     int ssp_coarse_pops = 0;     // MUX_SSP_COARSE_POPS [0, 1e9]: long-search pop limit at coarse levels
     bool ssp_serial = false;     // MUX_SSP_SERIAL=1: one warp search at a time
