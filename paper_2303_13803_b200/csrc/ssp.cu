@@ -2001,16 +2001,10 @@ __global__ void __launch_bounds__(NT, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef, i
             const int32_t jm = (int32_t)(best & kIdxMask);
             const int64_t dmin = (int64_t)(best >> kSH);
             const int32_t i = rocr[jm];
-            if (i < 0) { jf = jm; D = dmin; break; }
-            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (tid == 0) {
-                colof[i] = jm;
-#pragma unroll
-                for (int t = 0; t < kTieMax; ++t)
-                    if (t < nt) colof[rocr[tk[t] & kIdxMask]] = (int32_t)(tk[t] & kIdxMask);
-            }
+            // this step's loads first (a free winner ends the search below; its
+            // loads read the zero row), the bookkeeping after them
             const long long tA = tm ? clock64() : 0;
-            const wt_t* Ai = rowp(L, i);
+            const wt_t* Ai = i >= 0 ? rowp(L, i) : L.zrow;
             wt_t av[CC];
 #pragma unroll
             for (int u = 0; u < CC; ++u) {
@@ -2034,6 +2028,15 @@ __global__ void __launch_bounds__(NT, 1) ssp_rkey1_kernel(Lvl L, int32_t ndef, i
                         avt[t][u] = j < m ? __ldg(At + j) : 0;
                     }
                 }
+            }
+            asm volatile("" ::: "memory");
+            if (i < 0) { jf = jm; D = dmin; break; }
+            if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (tid == 0) {
+                colof[i] = jm;
+#pragma unroll
+                for (int t = 0; t < kTieMax; ++t)
+                    if (t < nt) colof[it[t]] = (int32_t)(tk[t] & kIdxMask);
             }
 #pragma unroll
             for (int u = 0; u < CC; ++u)
