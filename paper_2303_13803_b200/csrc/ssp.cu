@@ -2471,6 +2471,15 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         L.m = (int32_t)nr.size();
         L.rows = nr;
         L.cols = nc;
+        if (T.ssp_cperm && nc.size() > 64) {
+            // store the level's columns in a golden-ratio stride order: columns next to
+            // each other in key order (equal scores, often) then sit in different warps
+            // and CTAs of the long-path kernels, whose tie batching sees only warp minima
+            const int64_t mm = (int64_t)nc.size();
+            int64_t S = ((int64_t)(mm * 0.6180339887) | 1);
+            while (std::gcd(S, mm) != 1) S += 2;
+            for (int64_t k = 0; k < mm; ++k) L.cols[(size_t)((k * S) % mm)] = nc[(size_t)k];
+        }
         lv.push_back(L);
         cur_r = nr;
         cur_c = nc;
