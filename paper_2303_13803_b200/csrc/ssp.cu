@@ -241,10 +241,24 @@ __device__ void refresh_row(const Lvl& L, int32_t i) {
 }
 
 // One warp per row: initial candidate records of a level.
-__global__ void __launch_bounds__(256) cand_kernel(Lvl L) {
+// Padding rows [plo, phi) are all-zero rows, so they share one record: only
+// row plo is built here and pad_copy_kernel replicates it.
+__global__ void __launch_bounds__(256) cand_kernel(Lvl L, int32_t plo, int32_t phi) {
     const int32_t wid = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int32_t nw = (int32_t)((gridDim.x * (int64_t)blockDim.x) >> 5);
-    for (int32_t i = wid; i < L.m; i += nw) refresh_row(L, i);
+    for (int32_t i = wid; i < L.m; i += nw)
+        if (i <= plo || i >= phi) refresh_row(L, i);
+}
+
+__global__ void pad_copy_kernel(Lvl L, int32_t plo, int32_t phi) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t rows = (int64_t)(phi - plo - 1);
+    if (t >= rows * KC) return;
+    const int32_t i = plo + 1 + (int32_t)(t / KC);
+    const int32_t k = (int32_t)(t % KC);
+    L.cj[(int64_t)i * KC + k] = L.cj[(int64_t)plo * KC + k];
+    L.ca[(int64_t)i * KC + k] = L.ca[(int64_t)plo * KC + k];
+    if (k == 0) L.tau[i] = L.tau[plo];
 }
 
 // ---------------------------------------------------------------------------
@@ -2694,7 +2708,18 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
                 L.A, L.lda, L.nreal, L.zrow, m, reinterpret_cast<int32_t*>(B + o_sub[l]), pic, mc, chunk, L.p);
             launches += 3;
         }
-        cand_kernel<<<(unsigned)std::min<int64_t>(((int64_t)m * 32 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(L);
+        {
+            // padding rows share one record (built once, then copied)
+            const int32_t cplo = lv[l].phi > lv[l].plo ? lv[l].plo : m, cphi = lv[l].phi > lv[l].plo ? lv[l].phi : m;
+            const int64_t built = (int64_t)m - std::max<int32_t>(0, cphi - cplo - 1);
+            cand_kernel<<<(unsigned)std::min<int64_t>((built * 32 + 255) / 256, (int64_t)ctx->num_sms * 16), 256, 0, st>>>(
+                L, cplo, cphi);
+            if (cphi - cplo > 1) {
+                const int64_t tot = (int64_t)(cphi - cplo - 1) * KC;
+                pad_copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(L, cplo, cphi);
+                ++launches;
+            }
+        }
         launches += 3;
         double ms_setup = 0;
         if (verbose) {
