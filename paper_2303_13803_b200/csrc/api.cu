@@ -87,7 +87,7 @@ const Tuning& tuning() {
         t.auc_restage = knob("MUX_RESTAGE", 0, 0, 2, err);
         t.auc_order = knob("MUX_ORDER", 1, 0, 2, err);
         t.auc_no_smem = knob("MUX_NO_SMEM", 0, 0, 1, err) == 1;
-        t.mlp_prefetch = knob("MUX_MLP_PREFETCH", 0, 0, 1, err) == 1;
+        t.mlp_prefetch = knob("MUX_MLP_PREFETCH", t.mlp_prefetch ? 1 : 0, 0, 1, err) == 1;
     }
     t.error = !err.empty();
     if (t.error) set_error("bad tuning knob: " + err);

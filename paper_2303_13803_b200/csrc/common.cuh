@@ -86,7 +86,7 @@ struct Tuning {
     int auc_async_phases = 1 << 20;   // MUX_ASYNC_PHASES [0, 2^20]
     int auc_fresh = 1, auc_restage = 0, auc_order = 1;   // MUX_FRESH / MUX_RESTAGE / MUX_ORDER [0, 2]
     bool auc_no_smem = false;    // MUX_NO_SMEM=1: global-memory auction path
-    bool mlp_prefetch = false;   // MUX_MLP_PREFETCH=1
+    bool mlp_prefetch = true;    // MUX_MLP_PREFETCH=0: each tile loads its inputs when it builds h1 (no register prefetch)
     bool error = false;          // an out-of-range value was given
 };
 // Current knob values; *err set to a message when a value is out of range.
