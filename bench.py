@@ -454,11 +454,11 @@ def run_ours(args, rank, world, local_rank):
             ts.append(e0.elapsed_time(e1))
         mlp_ms = sorted(ts)[len(ts) // 2]
         flops = 2.0 * 64 * 64 * 2 * n * m + 4.0 * 64 * n * m
-        issued = 2.0 * 2 * 144 * 64 * n * m          # tensor flops issued: K = 64 hi + 64 lo + 16 bias per layer
+        issued = 2.0 * (144 + 128) * 64 * n * m      # tensor flops issued: K = 64 hi + 64 lo (+ 16 bias in layer 2)
         mlp_line = {"ms": mlp_ms, "tflops": flops / (mlp_ms / 1e3) / 1e12, "flops": flops,
                     "tensor_tflops_issued": issued / (mlp_ms / 1e3) / 1e12,
                     "note": "algorithmic flops (16.6 kFLOP/pair); layers 2-3 as tcgen05 kind::f16 M128 N64, "
-                            "split fp16 activations (hi + lo) + bias column: K = 144, fp32 TMEM accumulate"}
+                            "split fp16 activations (hi + lo): K = 144 / 128, layer 3 A operand in TMEM, fp32 TMEM accumulate"}
 
     if rank != 0:
         return

@@ -21,4 +21,4 @@ for _ in range(10):
     ts.append(e0.elapsed_time(e1))
 ms = sorted(ts)[5]
 fl = (2.0 * 64 * 64 * 2 + 4.0 * 64) * n * m
-print(f"mlp {n}x{m}: {ms:.3f} ms, {fl / ms / 1e9:.1f} TFLOP/s algorithmic, {2.0 * 2 * 144 * 64 * n * m / ms / 1e9:.1f} issued")
+print(f"mlp {n}x{m}: {ms:.3f} ms, {fl / ms / 1e9:.1f} TFLOP/s algorithmic, {2.0 * (144 + 128) * 64 * n * m / ms / 1e9:.1f} issued")
