@@ -1293,7 +1293,8 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     int par = 0;
     uint32_t ph = 0;
     uint64_t cand2 = kNoKey;
-    unsigned long long steps = 0, pfhits = 0, rounds = 0;
+    unsigned long long steps = 0, pfhits = 0, rounds = 0, walk = 0;
+    long long wcyc = 0;
     uint64_t tk[kTieMax];
     int nt = 0;
     const bool tm = (push & 16) != 0;
@@ -1526,18 +1527,26 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                     L.p[c0 + jj] = pj + (D - dj);
                 }
             }
-            // the path: predecessors live in their owners' shared memory
+            // the path walk reads every column's predecessor: gather them into CTA 0
+            // first (into its price table, unused until the next search reloads it),
+            // so each hop is a local shared-memory read instead of a DSMEM round trip
+            int32_t* predall = reinterpret_cast<int32_t*>(psr);
+            int32_t* dst = cluster.map_shared_rank(predall, 0);
+            for (int32_t jj = tid; jj < nloc; jj += NT) dst[c0 + jj] = pred[jj];
+            cluster.sync();
             if (rank == 0 && tid == 0) {
+                const long long tw = tm ? clock64() : 0;
                 int32_t j = jf;
                 while (true) {
-                    const int owner = j / mc;
-                    const int32_t ii = cluster.map_shared_rank(pred, owner)[j - owner * mc];
+                    const int32_t ii = predall[j];
                     const int32_t jn = (ii == s) ? -1 : colof[ii];
                     L.roc[j] = ii;
                     L.cor[ii] = j;
+                    ++walk;
                     if (ii == s) break;
                     j = jn;
                 }
+                if (tm) wcyc += clock64() - tw;
             }
         }
         __threadfence();
@@ -1560,8 +1569,12 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     }
     if (tm && rank == 0 && tid == 0)
         for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)&L.cnt->xcyc[k], (unsigned long long)tcyc[k]);
-    if (tm && rank == 0 && tid == 0)
+    if (tm && rank == 0 && tid == 0) {
         for (int k = 0; k < 5; ++k) atomicAdd(&L.cnt->xt[k], txt[k]);
+        atomicAdd(&L.cnt->xwalk, walk);
+        atomicAdd(&L.cnt->xwalkcyc, (unsigned long long)wcyc);
+        atomicAdd(&L.cnt->xsearch, (unsigned long long)ndef);
+    }
 }
 
 // Register-key kernel for levels too large to replicate prices and owners
