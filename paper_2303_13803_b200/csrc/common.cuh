@@ -73,6 +73,7 @@ struct Tuning {
     int ssp_taildef = 4;         // MUX_SSP_TAILDEF [0, 4096]: retried row lists up to this size go to the long-path kernel
     bool ssp_wide = true;        // MUX_SSP_WIDE=0: no 16-CTA clusters for the slice kernel (m > 16,384)
     bool ssp_cperm = true;       // MUX_SSP_CPERM=0: coarse levels store their columns in key order, not a stride order
+    bool ssp_lwalk = true;       // MUX_SSP_LWALK=0: the slice kernel's path walk reads DSMEM / global per hop
     int ssp_seq = 64;            // MUX_SSP_SEQ [0, 4096]: levels up to this size skip the parallel passes
     int ssp_dorder = 1;          // MUX_SSP_DORDER [0, 2]: long searches in defer order / ascending / descending row key
     const char* ssp_dump = nullptr;

@@ -1899,7 +1899,34 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                     L.p[c0 + jj] = pj + (D - dj);
                 }
             }
-            if (rank == 0 && tid == 0) {
+            if (flags & 128) {
+                // local walk: every column's (predecessor, predecessor's old column) pair,
+                // 16 bits each, gathered into CTA 0 (launched with 4 m more bytes) in one
+                // parallel pass, so a hop is a shared-memory read instead of a DSMEM read
+                // plus a global one
+                uint32_t* ps = reinterpret_cast<uint32_t*>(smem + 4 * (size_t)mc + 64);
+                uint32_t* dst = cluster.map_shared_rank(ps, 0);
+                for (int32_t jj = tid; jj < nloc; jj += NT) {
+                    const int32_t ii = pred[jj];
+                    const int32_t jo = ii == s ? 0xFFFF : __ldcg(L.cor + ii);
+                    dst[c0 + jj] = ((uint32_t)ii << 16) | (uint32_t)(jo & 0xFFFF);
+                }
+                cluster.sync();
+                if (rank == 0 && tid == 0) {
+                    const long long tw = tm ? clock64() : 0;
+                    int32_t j = jf;
+                    while (true) {
+                        const uint32_t v = ps[j];
+                        const int32_t ii = (int32_t)(v >> 16);
+                        L.roc[j] = ii;
+                        L.cor[ii] = j;
+                        ++walk;
+                        if (ii == s) break;
+                        j = (int32_t)(v & 0xFFFF);
+                    }
+                    if (tm) wcyc += clock64() - tw;
+                }
+            } else if (rank == 0 && tid == 0) {
                 const long long tw = tm ? clock64() : 0;
                 int32_t j = jf;
                 while (true) {
@@ -2589,10 +2616,10 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<1, CL, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_kernel<2, CL, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024 - push_b8)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_slice_kernel<4, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<16, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<16, CL, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<1, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<2, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
     MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey1_kernel<3, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(xs_budget - 1024)));
@@ -2614,9 +2641,9 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, 16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, 16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, 16, 512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<3, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<6, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        MUX_CUDA_TRY(cudaFuncSetAttribute(ssp_rkey_slice_kernel<10, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
@@ -2625,7 +2652,7 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         at[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3(16);
         cfg.blockDim = dim3(512);
-        cfg.dynamicSmemBytes = 64 * 1024;
+        cfg.dynamicSmemBytes = 200 * 1024;
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int nclusters = 0;
@@ -2881,17 +2908,26 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
                 // register keys with (key, owner | price) pushes: no replicated tables
                 const size_t rs_bytes = 4ull * mcl + 64;
                 const int32_t m16 = (m + 15) / 16;
+                // local path walk (flag 128) when 16-bit indices and 4 m more bytes per CTA fit
+                const bool lw = n <= 65535 && T.ssp_lwalk;
                 if (wide_ok && m16 <= 512 * 10) {
                     // 16-CTA clusters (non-portable size): half the columns per CTA
                     // (10k x 40k: 156 -> 143 ms of long paths, profiles/r03/cluster16_slice.log)
-                    const size_t rs16 = 4ull * m16 + 64;
-                    if (m16 <= 512 * 3) ssp_rkey_slice_kernel<3, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, cpush);
-                    else if (m16 <= 512 * 6) ssp_rkey_slice_kernel<6, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, cpush);
-                    else ssp_rkey_slice_kernel<10, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, cpush);
-                } else if (mcl <= 512 * 3) ssp_rkey_slice_kernel<3, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
-                else if (mcl <= 512 * 6) ssp_rkey_slice_kernel<6, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
-                else if (mcl <= 512 * 10) ssp_rkey_slice_kernel<10, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
-                else ssp_rkey_slice_kernel<16, CL, 512><<<CL, 512, rs_bytes, st>>>(L, ndef_total, pl, cpush);
+                    size_t rs16 = 4ull * m16 + 64;
+                    int32_t f16 = cpush;
+                    if (lw && rs16 + 4ull * m + 64 <= 200ull * 1024) { rs16 += 4ull * m + 64; f16 |= 128; }
+                    if (m16 <= 512 * 3) ssp_rkey_slice_kernel<3, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, f16);
+                    else if (m16 <= 512 * 6) ssp_rkey_slice_kernel<6, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, f16);
+                    else ssp_rkey_slice_kernel<10, 16, 512><<<16, 512, rs16, st>>>(L, ndef_total, pl, f16);
+                } else {
+                    size_t rsb = rs_bytes;
+                    int32_t f8 = cpush;
+                    if (lw && rsb + 4ull * m + 64 <= 200ull * 1024) { rsb += 4ull * m + 64; f8 |= 128; }
+                    if (mcl <= 512 * 3) ssp_rkey_slice_kernel<3, CL, 512><<<CL, 512, rsb, st>>>(L, ndef_total, pl, f8);
+                    else if (mcl <= 512 * 6) ssp_rkey_slice_kernel<6, CL, 512><<<CL, 512, rsb, st>>>(L, ndef_total, pl, f8);
+                    else if (mcl <= 512 * 10) ssp_rkey_slice_kernel<10, CL, 512><<<CL, 512, rsb, st>>>(L, ndef_total, pl, f8);
+                    else ssp_rkey_slice_kernel<16, CL, 512><<<CL, 512, rsb, st>>>(L, ndef_total, pl, f8);
+                }
             } else if (slice_ok) {
                 if (m <= CL * CTHREADS * 4) ssp_slice_kernel<4, CL><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
                 else ssp_slice_kernel<CCOLS, CL><<<CL, CTHREADS, cl_bytes, st>>>(L, ndef_total, pl);
