@@ -63,12 +63,12 @@ struct Tuning {
     int ssp_coarse_pops = 0;     // MUX_SSP_COARSE_POPS [0, 1e9]: long-search pop limit at coarse levels
     bool ssp_serial = false;     // MUX_SSP_SERIAL=1: one warp search at a time
     bool ssp_pf = false;         // MUX_SSP_PF=1: TMA prefetch of the runner-up's row slice in the long-path kernel
-    bool ssp_l2pf = false;       // MUX_SSP_L2PF=1: L2 prefetch of every warp-minimum candidate's row slice
+    int ssp_l2pf = 0;            // MUX_SSP_L2PF [0, 1]: L2 prefetch of every warp-minimum candidate's row slice
     bool ssp_ties = true;        // MUX_SSP_TIES=0: one pop per exchange step (no tie batching)
     bool ssp_cluster = true;     // MUX_SSP_CLUSTER=0: single-CTA / single-warp long paths
     bool ssp_sparsex = false;    // MUX_SSP_SPARSEX=1: single-warp sparse long paths
     int ssp_rslice = 1;          // MUX_SSP_RSLICE [0, 2]: 0 = large levels on the shared-memory sliced kernel, 2 = every cluster level on it
-    int ssp_ct1 = 512;           // MUX_SSP_CT1 {512, 1024}: threads of the single-SM long-path kernel (levels <= 3072)
+    int ssp_ct1 = 512;           // MUX_SSP_CT1 {512, 1024}: threads of the single-SM long-path kernel (512: levels <= 3072)
     int ssp_ct = 256;            // MUX_SSP_CT {128, 256, 512, 1024}: threads per CTA of the long-path kernel
     int ssp_taildef = 4;         // MUX_SSP_TAILDEF [0, 4096]: retried row lists up to this size go to the long-path kernel
     bool ssp_wide = true;        // MUX_SSP_WIDE=0: no 16-CTA clusters for the slice kernel (m > 16,384)
@@ -76,8 +76,8 @@ struct Tuning {
     bool ssp_lwalk = true;       // MUX_SSP_LWALK=0: the slice kernel's path walk reads DSMEM / global per hop
     int ssp_seq = 64;            // MUX_SSP_SEQ [0, 4096]: levels up to this size skip the parallel passes
     int ssp_dorder = 1;          // MUX_SSP_DORDER [0, 2]: long searches in defer order / ascending / descending row key
-    const char* ssp_dump = nullptr;
-    const char* canon_dump = nullptr;   // MUX_CANON_DUMP=file: the canonicalisation host loop's inputs and output   // MUX_SSP_DUMP=dir: write each long-search batch's level state (analysis)
+    const char* ssp_dump = nullptr;     // MUX_SSP_DUMP=dir: write each long-search batch's level state (analysis)
+    const char* canon_dump = nullptr;   // MUX_CANON_DUMP=file: the canonicalisation host loop's inputs and output
     int ssp_one = 1300;          // MUX_SSP_ONE [0, 10240]: levels up to this size run long paths on one SM
     int auc_theta = 4;           // MUX_THETA [2, 64]: epsilon-scaling factor
     int auc_tail = -1;           // MUX_TAIL [-1, 2^20]: unassigned count that ends the Jacobi rounds (clamped to 16)
