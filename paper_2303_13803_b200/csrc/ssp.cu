@@ -131,6 +131,12 @@ struct Lvl {
     int32_t* xstamp;    // flags (uint8) when the tables live in global memory
     int32_t* xscol;     // scanned columns of the current search
     int32_t* xgap;      // global fallback: horizon gaps
+    // rank-neighbour L2 prefetch of the long-path kernel (level 0): a long search pops
+    // the rows of a contiguous key-rank window, so rows rpf ranks either side of the
+    // popped row are fetched into L2 a few steps ahead (rpf = 0: off)
+    const int32_t* rankof;   // [m] key rank of each row
+    const int32_t* rowat;    // [m] row of each key rank
+    int32_t rpf;
 };
 
 __device__ __forceinline__ const wt_t* rowp(const Lvl& L, int32_t i) {
@@ -1297,6 +1303,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
     long long wcyc = 0;
     uint64_t tk[kTieMax];
     int nt = 0;
+    int32_t rpf_rank = -1, rpf_row = -1;   // rank-neighbour prefetch pipeline (two lanes)
     const bool tm = (push & 16) != 0;
     long long tcyc[3] = {0, 0, 0};
     unsigned long long txt[5] = {0, 0, 0, 0, 0};
@@ -1401,6 +1408,20 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             asm volatile("" ::: "memory");
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
+            if (L.rpf > 0 && tid >= NT - 2) {
+                // two lanes of the last warp, one step per stage: prefetch the row found
+                // last step, look up the row rpf ranks away from last step's rank, load
+                // this step's rank (each load is consumed a step later, off the critical path)
+                if (rpf_row >= 0 && nloc > 0) {
+                    const wt_t* src = rowp(L, rpf_row) + c0;
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+                }
+                const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + (tid == NT - 1 ? L.rpf : -L.rpf);
+                rpf_row = rr >= 0 && rr < m ? __ldcg(L.rowat + rr) : -1;
+                rpf_rank = __ldcg(L.rankof + i);
+            }
             if (rank == 0 && tid == 0) {
                 colof[i] = jm;
 #pragma unroll
@@ -2570,7 +2591,7 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         o_rl[l] = take(4 * m + 64);
     }
     const size_t o_xd = take(8ull * n), o_xp = take(4ull * n), o_xs = take(4ull * n), o_xc = take(4ull * n + 256),
-                 o_xh = take(4ull * n);
+                 o_xh = take(4ull * n), o_rank = take(4ull * n), o_rowat = take(4ull * n);
     MUX_TRY(ctx->ssp.ensure(off));
     char* B = ctx->ssp.as<char>();
     Cnt* cnt = reinterpret_cast<Cnt*>(B + o_cnt);
@@ -2589,6 +2610,13 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
     }
     for (int l = 0; l + 1 < nl; ++l)
         MUX_CUDA_TRY(cudaMemcpyAsync(B + o_sub[l], lv[l].sub.data(), 4ull * lv[l].sub.size(), cudaMemcpyHostToDevice, st));
+    std::vector<int32_t> rank0;
+    if (T.ssp_rpf > 0) {   // level 0's key ranks for the rank-neighbour prefetch
+        rank0.assign(n, 0);
+        for (int32_t k = 0; k < n; ++k) rank0[ro[k]] = k;
+        MUX_CUDA_TRY(cudaMemcpyAsync(B + o_rank, rank0.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+        MUX_CUDA_TRY(cudaMemcpyAsync(B + o_rowat, ro.data(), 4ull * n, cudaMemcpyHostToDevice, st));
+    }
 
     const size_t psmem = sizeof(WTab) * PWARPS;
     // exclusive pass: per-column tables in shared memory when they fit
@@ -2707,6 +2735,9 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         L.xstamp = reinterpret_cast<int32_t*>(B + o_xs);
         L.xscol = reinterpret_cast<int32_t*>(B + o_xc);
         L.xgap = reinterpret_cast<int32_t*>(B + o_xh);
+        L.rankof = reinterpret_cast<const int32_t*>(B + o_rank);
+        L.rowat = reinterpret_cast<const int32_t*>(B + o_rowat);
+        L.rpf = (l == 0 && T.ssp_rpf > 0 && 4ull * m * m > (96ull << 20)) ? T.ssp_rpf : 0;
         // queue order: a stride permutation spreads concurrent searches over the level
         int32_t stride = 7919;
         while (std::gcd(stride, m) != 1) stride += 2;
