@@ -74,6 +74,7 @@ const Tuning& tuning() {
         t.canon_dump = getenv("MUX_CANON_DUMP");
         t.ssp_seq = knob("MUX_SSP_SEQ", t.ssp_seq, 0, 4096, err);
         t.ssp_rpf = knob("MUX_SSP_RPF", t.ssp_rpf, 0, 64, err);
+        t.ssp_rpf_mb = knob("MUX_SSP_RPF_MB", t.ssp_rpf_mb, 0, 65536, err);
         t.ssp_lwalk = knob("MUX_SSP_LWALK", t.ssp_lwalk ? 1 : 0, 0, 1, err) == 1;
         t.ssp_cperm = knob("MUX_SSP_CPERM", t.ssp_cperm ? 1 : 0, 0, 1, err) == 1;
         t.ssp_wide = knob("MUX_SSP_WIDE", t.ssp_wide ? 1 : 0, 0, 1, err) == 1;

@@ -75,6 +75,7 @@ struct Tuning {
     bool ssp_cperm = true;       // MUX_SSP_CPERM=0: coarse levels store their columns in key order, not a stride order
     bool ssp_lwalk = true;       // MUX_SSP_LWALK=0: the slice kernel's path walk reads DSMEM / global per hop
     int ssp_rpf = 16;            // MUX_SSP_RPF [0, 64]: rank-neighbour L2 prefetch distance of the long-path kernel (0 = off)
+    int ssp_rpf_mb = 64;         // MUX_SSP_RPF_MB [0, 65536]: levels whose matrix exceeds this many MiB use it
     int ssp_seq = 64;            // MUX_SSP_SEQ [0, 4096]: levels up to this size skip the parallel passes
     int ssp_dorder = 1;          // MUX_SSP_DORDER [0, 2]: long searches in defer order / ascending / descending row key
     const char* ssp_dump = nullptr;     // MUX_SSP_DUMP=dir: write each long-search batch's level state (analysis)

@@ -1419,8 +1419,13 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
                 }
                 const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + (tid == NT - 1 ? L.rpf : -L.rpf);
-                rpf_row = rr >= 0 && rr < m ? __ldcg(L.rowat + rr) : -1;
-                rpf_rank = __ldcg(L.rankof + i);
+                if (L.rankof) {   // level 0: rows in the caller's order
+                    rpf_row = rr >= 0 && rr < m ? __ldcg(L.rowat + rr) : -1;
+                    rpf_rank = __ldcg(L.rankof + i);
+                } else {          // coarse levels index their rows in key order
+                    rpf_row = rr >= 0 && rr < m ? rr : -1;
+                    rpf_rank = i;
+                }
             }
             if (rank == 0 && tid == 0) {
                 colof[i] = jm;
@@ -2735,9 +2740,9 @@ int MUX_SSP_IMPL(mux_ctx_t* ctx, const wt_t* W, int64_t ldw, int32_t N, int32_t 
         L.xstamp = reinterpret_cast<int32_t*>(B + o_xs);
         L.xscol = reinterpret_cast<int32_t*>(B + o_xc);
         L.xgap = reinterpret_cast<int32_t*>(B + o_xh);
-        L.rankof = reinterpret_cast<const int32_t*>(B + o_rank);
-        L.rowat = reinterpret_cast<const int32_t*>(B + o_rowat);
-        L.rpf = (l == 0 && T.ssp_rpf > 0 && 4ull * m * m > (96ull << 20)) ? T.ssp_rpf : 0;
+        L.rankof = l == 0 ? reinterpret_cast<const int32_t*>(B + o_rank) : nullptr;
+        L.rowat = l == 0 ? reinterpret_cast<const int32_t*>(B + o_rowat) : nullptr;
+        L.rpf = (T.ssp_rpf > 0 && sizeof(wt_t) * m * m > ((size_t)T.ssp_rpf_mb << 20)) ? T.ssp_rpf : 0;
         // queue order: a stride permutation spreads concurrent searches over the level
         int32_t stride = 7919;
         while (std::gcd(stride, m) != 1) stride += 2;
