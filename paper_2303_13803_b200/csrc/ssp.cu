@@ -1773,6 +1773,7 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
     constexpr int TM = kTieMaxSlice;
     ulonglong2 te[TM];
     int nt = 0;
+    int32_t rpf_rank = -1, rpf_row = -1;   // rank-neighbour prefetch pipeline (two lanes)
     extern __shared__ __align__(16) unsigned char smem[];
     int32_t* pred = reinterpret_cast<int32_t*>(smem);   // [mc] predecessor rows (local)
     cg::cluster_group cluster = cg::this_cluster();
@@ -1863,6 +1864,23 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                         const int32_t jj = tid + u * NT;
                         avt[t][u] = jj < nloc ? __ldg(At + c0 + jj) : 0;
                     }
+                }
+            }
+            if (L.rpf > 0 && tid >= NT - 2) {
+                // rank-neighbour L2 prefetch pipeline (as in ssp_rkey_kernel)
+                if (rpf_row >= 0 && nloc > 0) {
+                    const wt_t* src = rowp(L, rpf_row) + c0;
+                    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+                    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+                }
+                const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + (tid == NT - 1 ? L.rpf : -L.rpf);
+                if (L.rankof) {
+                    rpf_row = rr >= 0 && rr < m ? __ldcg(L.rowat + rr) : -1;
+                    rpf_rank = __ldcg(L.rankof + i);
+                } else {
+                    rpf_row = rr >= 0 && rr < m ? rr : -1;
+                    rpf_rank = i;
                 }
             }
             if (jm >= c0 && jm < c0 + nloc) {
