@@ -1264,6 +1264,9 @@ ssp_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit) {
 // ---------------------------------------------------------------------------
 
 constexpr uint64_t kTop = 1ull << 63;
+#ifndef RPF_LANES
+#define RPF_LANES 2   // lanes of the rank-neighbour prefetch (two per distance: up and down)
+#endif
 
 template <int CC, int CLS, int NT>
 __global__ void __cluster_dims__(CLS, 1, 1) __launch_bounds__(NT, 1)
@@ -1408,7 +1411,7 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
             asm volatile("" ::: "memory");
             if (i < 0) { jf = jm; D = dmin; break; }
             if (pop_limit > 0 && (pops += 1 + nt) > pop_limit) { abandon = true; jf = -1; D = 0; break; }
-            if (L.rpf > 0 && tid >= NT - 2) {
+            if (L.rpf > 0 && tid >= NT - RPF_LANES) {
                 // two lanes of the last warp, one step per stage: prefetch the row found
                 // last step, look up the row rpf ranks away from last step's rank, load
                 // this step's rank (each load is consumed a step later, off the critical path)
@@ -1418,7 +1421,10 @@ ssp_rkey_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t push) {
                     const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
                 }
-                const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + (tid == NT - 1 ? L.rpf : -L.rpf);
+                // lane NT-1-k: distance (k / 2 + 1) * rpf / (RPF_LANES / 2), up for even k, down for odd
+                const int kq = NT - 1 - tid;
+                const int32_t dist = (int32_t)(((kq >> 1) + 1) * L.rpf / (RPF_LANES / 2));
+                const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + ((kq & 1) ? -dist : dist);
                 if (L.rankof) {   // level 0: rows in the caller's order
                     rpf_row = rr >= 0 && rr < m ? __ldcg(L.rowat + rr) : -1;
                     rpf_rank = __ldcg(L.rankof + i);
@@ -1866,7 +1872,7 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                     }
                 }
             }
-            if (L.rpf > 0 && tid >= NT - 2) {
+            if (L.rpf > 0 && tid >= NT - RPF_LANES) {
                 // rank-neighbour L2 prefetch pipeline (as in ssp_rkey_kernel)
                 if (rpf_row >= 0 && nloc > 0) {
                     const wt_t* src = rowp(L, rpf_row) + c0;
@@ -1874,7 +1880,10 @@ ssp_rkey_slice_kernel(Lvl L, int32_t ndef, int32_t pop_limit, int32_t flags) {
                     const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + nloc) + 15) & ~(uintptr_t)15;
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
                 }
-                const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + (tid == NT - 1 ? L.rpf : -L.rpf);
+                // lane NT-1-k: distance (k / 2 + 1) * rpf / (RPF_LANES / 2), up for even k, down for odd
+                const int kq = NT - 1 - tid;
+                const int32_t dist = (int32_t)(((kq >> 1) + 1) * L.rpf / (RPF_LANES / 2));
+                const int32_t rr = rpf_rank < 0 ? -1 : rpf_rank + ((kq & 1) ? -dist : dist);
                 if (L.rankof) {
                     rpf_row = rr >= 0 && rr < m ? __ldcg(L.rowat + rr) : -1;
                     rpf_rank = __ldcg(L.rankof + i);
