@@ -29,13 +29,13 @@ struct Canon {
     std::vector<uint32_t> stamp;      // column: epoch of the search that visited it, kLocked once locked
     std::vector<uint32_t> dead;       // row: dead-row epoch (see run())
     std::vector<int32_t> parent;
-    std::vector<int32_t> frontier, nxt, explored;        // BFS levels and rows, reused across searches
+    std::vector<int32_t> queue;                          // BFS queue of rows (its prefix: the explored rows)
     std::vector<std::pair<int32_t, int32_t>> moves;      // the applied path
     uint32_t epoch = 0, dep = 0;
     long long searches = 0, visits = 0, fails = 0, pruned = 0;
 
     Canon(const TightGraph& g, std::vector<int32_t>& c)
-        : G(g), col(c), row_of_col(g.n), stamp(g.n, 0), dead(g.n, 0), parent(g.n, -1) {
+        : G(g), col(c), row_of_col(g.n), stamp(g.n, 0), dead(g.n, 0), parent(g.n, -1), queue((size_t)g.n + 1) {
         for (int32_t i = 0; i < G.n; ++i) row_of_col[col[i]] = i;
     }
     bool seen(int32_t j) const { return stamp[j] >= epoch; }   // this search, or locked
@@ -47,10 +47,15 @@ struct Canon {
         if (dead[start_row] == dep) { ++fails; ++pruned; return false; }
         ++epoch;
         stamp[banned_col] = epoch;
-        frontier.assign(1, start_row);
-        explored.assign(1, start_row);
-        nxt.clear();
+        // one FIFO queue: the same level-by-level order as a frontier / next-frontier
+        // pair, and its prefix is the set of explored rows
+        int32_t* q = queue.data();
+        int32_t head = 0, tail = 0;
+        q[tail++] = start_row;
         bool found = false, z_done = false, zp_done = false;
+        const int32_t* ent = G.ent->data();
+        const int64_t* off = G.off->data();
+        const int32_t* cnt = G.cnt->data();
         auto visit = [&](int32_t r, int32_t j) -> bool {
             if (seen(j)) return false;
             ++visits;
@@ -58,39 +63,32 @@ struct Canon {
             parent[j] = r;
             if (j == target_col) return true;
             const int32_t r2 = row_of_col[j];
-            if (r2 != banned_row && dead[r2] != dep) {
-                nxt.push_back(r2);
-                explored.push_back(r2);
-            }
+            if (r2 != banned_row && dead[r2] != dep) q[tail++] = r2;
             return false;
         };
-        while (!frontier.empty() && !found) {
-            nxt.clear();
-            for (int32_t r : frontier) {
-                if (r >= G.N) {                      // padding row: tight to Z
-                    if (!z_done) {
-                        z_done = true;   // every later padding row finds Z visited
-                        for (int32_t j : G.Z)
-                            if (visit(r, j)) { found = true; break; }
-                    }
-                } else {
-                    const int32_t* e = G.ent->data() + (*G.off)[r];
-                    const int32_t k = (*G.cnt)[r];
-                    for (int32_t t = 0; t < k && !found; ++t)
-                        if (visit(r, e[t] & 0x7fffffff)) found = true;
-                    if (!found && G.padrow_tight.size() && G.padrow_tight[r] && !zp_done) {
-                        zp_done = true;
-                        for (int32_t j : G.Zpad)
-                            if (visit(r, j)) { found = true; break; }
-                    }
+        while (head < tail && !found) {
+            const int32_t r = q[head++];
+            if (r >= G.N) {                      // padding row: tight to Z
+                if (!z_done) {
+                    z_done = true;   // every later padding row finds Z visited
+                    for (int32_t j : G.Z)
+                        if (visit(r, j)) { found = true; break; }
                 }
-                if (found) break;
+            } else {
+                const int32_t* e = ent + off[r];
+                const int32_t k = cnt[r];
+                for (int32_t t = 0; t < k && !found; ++t)
+                    if (visit(r, e[t] & 0x7fffffff)) found = true;
+                if (!found && G.padrow_tight.size() && G.padrow_tight[r] && !zp_done) {
+                    zp_done = true;
+                    for (int32_t j : G.Zpad)
+                        if (visit(r, j)) { found = true; break; }
+                }
             }
-            frontier.swap(nxt);
         }
         if (!found) {
             ++fails;
-            for (int32_t r : explored) dead[r] = dep;
+            for (int32_t t = 0; t < tail; ++t) dead[q[t]] = dep;
             return false;
         }
         // reconstruct from the target back to start_row, then apply
