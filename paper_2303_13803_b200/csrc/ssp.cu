@@ -249,7 +249,10 @@ __device__ void refresh_row(const Lvl& L, int32_t i) {
 // One warp per row: initial candidate records of a level.
 // Padding rows [plo, phi) are all-zero rows, so they share one record: only
 // row plo is built here and pad_copy_kernel replicates it.
-__global__ void __launch_bounds__(256) cand_kernel(Lvl L, int32_t plo, int32_t phi) {
+#ifndef CAND_MINB
+#define CAND_MINB 5   // 48 registers: more resident warps for this latency-bound scan (level-0 setup 0.69 -> 0.63 ms)
+#endif
+__global__ void __launch_bounds__(256, CAND_MINB) cand_kernel(Lvl L, int32_t plo, int32_t phi) {
     const int32_t wid = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
     const int32_t nw = (int32_t)((gridDim.x * (int64_t)blockDim.x) >> 5);
     for (int32_t i = wid; i < L.m; i += nw)
